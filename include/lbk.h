@@ -1,0 +1,271 @@
+/* include/lbk.h -- C ABI of the B200 sparse backend ("lbk").
+ *
+ * This is the drop-in boundary for the reference's SpMV/Krylov hot path
+ * (reference = /root/reference/proj, "larch").  Every entry point names the
+ * reference interface it replaces (file:line, relative to that tree).
+ *
+ * Conventions
+ *  - C linkage, plain pointers and sizes, no C++ or torch types.
+ *  - Every function returns an lbk_status; lbk_last_error(ctx) gives the
+ *    message (ctx may be NULL for errors raised before a context exists).
+ *    Status codes map 1:1 onto the reference's exception taxonomy
+ *    (include/larch/core/error.hpp:16-131).  No exception crosses the ABI.
+ *  - Matrix descriptors are plain structs of DEVICE pointers borrowed (not
+ *    owned) by the call.  Vectors are device pointers.  Kernels never
+ *    allocate their outputs (reference kernels.hpp:76-97 contract).
+ *  - One lbk_ctx is bound to one device and one CUDA stream; calls on a ctx
+ *    are stream-ordered and not re-entrant across threads.  SpMV / BLAS-1 /
+ *    conversion calls are asynchronous on that stream; calls that return a
+ *    host value (dot/nrm2 to host, solve, ell_width, sellp_plan, validate)
+ *    synchronise the stream before returning.  The reference's wrappers are
+ *    synchronous (dispatch.cpp:112-117); lbk_sync(ctx) restores that.
+ *  - Indices are int32 (reference SPEC.md:359); nnz is int64 in the
+ *    descriptors so sizes above 2^31 are rejected cleanly, not wrapped.
+ */
+#ifndef LBK_H
+#define LBK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------- status */
+/* error.hpp:16-131 -> status codes */
+typedef enum lbk_status {
+    LBK_OK = 0,
+    LBK_SHAPE_ERROR = 1,           /* ShapeError           error.hpp:49 */
+    LBK_PLACEMENT_ERROR = 2,       /* PlacementError       error.hpp:63 */
+    LBK_TYPE_ERROR = 3,            /* TypeError            error.hpp:56 */
+    LBK_DISPATCH_ERROR = 4,        /* DispatchError        error.hpp:78 */
+    LBK_USAGE_ERROR = 5,           /* UsageError           error.hpp:71 */
+    LBK_CONFIGURATION_ERROR = 6,   /* ConfigurationError   error.hpp:23 */
+    LBK_OUT_OF_MEMORY = 7,         /* OutOfMemoryError     error.hpp:30 */
+    LBK_FORMAT_ERROR = 8,          /* FormatError          error.hpp:100 */
+    LBK_BREAKDOWN = 9,             /* BreakdownError       error.hpp:115 */
+    LBK_BENCHMARK_INTEGRITY = 10,  /* BenchmarkIntegrityError error.hpp:128 */
+    LBK_CUDA_ERROR = 20,           /* device/runtime failure (new) */
+    LBK_NCCL_ERROR = 21,           /* collective failure (new) */
+    LBK_INTERNAL = 99
+} lbk_status;
+
+typedef enum lbk_dtype { LBK_F64 = 0, LBK_F32 = 1 } lbk_dtype;
+
+/* ------------------------------------------------------------ context */
+/* Replaces the Executor seam: executor.hpp:130-170 (kind/synchronize/
+ * raw_alloc with arena capacity -> OutOfMemoryError) and create_executor
+ * executor.hpp:261-262. */
+typedef struct lbk_ctx_s* lbk_ctx;
+
+lbk_status lbk_ctx_create(int device, lbk_ctx* out);
+/* Bind to an existing cudaStream_t (e.g. torch.cuda.current_stream()). */
+lbk_status lbk_ctx_create_on_stream(int device, void* cuda_stream, lbk_ctx* out);
+lbk_status lbk_ctx_set_stream(lbk_ctx ctx, void* cuda_stream);
+lbk_status lbk_ctx_destroy(lbk_ctx ctx);
+const char* lbk_last_error(lbk_ctx ctx);
+/* Executor::synchronize (executor.hpp:146). */
+lbk_status lbk_sync(lbk_ctx ctx);
+/* Number of SMs, device id, arena accounting (executor.hpp:150-160). */
+lbk_status lbk_ctx_info(lbk_ctx ctx, int* device, int* num_sms,
+                        size_t* arena_capacity, size_t* arena_used);
+lbk_status lbk_ctx_set_arena_capacity(lbk_ctx ctx, size_t bytes);
+/* Executor::raw_alloc / raw_free (executor.cpp:254-279): device memory,
+ * 256-B aligned, LBK_OUT_OF_MEMORY past the arena capacity. */
+lbk_status lbk_alloc(lbk_ctx ctx, size_t bytes, void** out);
+lbk_status lbk_free(lbk_ctx ctx, void* ptr, size_t bytes);
+/* copy()/array_from_host/array_to_host (device_array.cpp:144-263); device
+ * to device across GPUs is a direct peer copy, not 3-hop master staging. */
+lbk_status lbk_memcpy_h2d(lbk_ctx ctx, void* dst, const void* src, size_t bytes);
+lbk_status lbk_memcpy_d2h(lbk_ctx ctx, void* dst, const void* src, size_t bytes);
+lbk_status lbk_memcpy_d2d(lbk_ctx ctx, void* dst, const void* src, size_t bytes);
+
+/* ---------------------------------------------------------- matrices */
+/* CsrMatrix (formats.hpp:65-76).  `tile_rows` is an optional load-balance
+ * plan from lbk_csr_plan(); when NULL the SpMV builds it per call. */
+typedef struct lbk_csr {
+    int32_t nrows, ncols;
+    int64_t nnz;
+    lbk_dtype dtype;
+    const int32_t* row_ptr;  /* nrows + 1 */
+    const int32_t* col_idx;  /* nnz */
+    const void* vals;        /* nnz, double or float */
+    const int32_t* tile_rows; /* optional plan, see lbk_csr_plan */
+    int32_t ntiles;
+} lbk_csr;
+
+/* CooMatrix (formats.hpp:49-60): sorted by (row, col), unique. */
+typedef struct lbk_coo {
+    int32_t nrows, ncols;
+    int64_t nnz;
+    lbk_dtype dtype;
+    const int32_t* row_idx;
+    const int32_t* col_idx;
+    const void* vals;
+    const int32_t* tile_starts; /* optional plan, see lbk_coo_plan */
+    int32_t ntiles;
+} lbk_coo;
+
+/* ELL, Ginkgo column-major (new): entry (r, j) at
+ * j*stride + r, padding column -1 / value 0. */
+typedef struct lbk_ell {
+    int32_t nrows, ncols;
+    int64_t nnz;      /* logical nonzeros (flop accounting) */
+    lbk_dtype dtype;
+    int32_t width;
+    int64_t stride;   /* >= nrows */
+    const int32_t* col_idx;  /* width * stride */
+    const void* vals;
+} lbk_ell;
+
+/* SELL-P (new; App. B): slice size S, entry (r, j) at
+ * (slice_sets[r/S] + j)*S + r%S, padding column -1 / value 0. */
+typedef struct lbk_sellp {
+    int32_t nrows, ncols;
+    int64_t nnz;
+    lbk_dtype dtype;
+    int32_t slice_size;
+    int32_t nslices;
+    const int32_t* slice_lengths; /* nslices */
+    const int32_t* slice_sets;    /* nslices + 1 */
+    const int32_t* col_idx;       /* slice_sets[nslices] * S */
+    const void* vals;
+} lbk_sellp;
+
+/* ------------------------------------------------------------- SpMV */
+/* spmv_csr / spmv_coo (kernels.hpp:94-97, api.cpp:113-140): y <- A x,
+ * overwrite, empty rows -> 0.  Shape checks raise LBK_SHAPE_ERROR
+ * (api.cpp:27-33); a descriptor dtype that does not match the entry point
+ * raises LBK_TYPE_ERROR.  The _adv variants are the north star's "advanced
+ * apply" y <- alpha A x + beta y (absent from the reference; beta == 0 does
+ * not read y). */
+lbk_status lbk_spmv_csr_f64(lbk_ctx, const lbk_csr* A, const double* x, double* y);
+lbk_status lbk_spmv_csr_f32(lbk_ctx, const lbk_csr* A, const float* x, float* y);
+lbk_status lbk_spmv_csr_adv_f64(lbk_ctx, double alpha, const lbk_csr* A,
+                                const double* x, double beta, double* y);
+lbk_status lbk_spmv_csr_adv_f32(lbk_ctx, float alpha, const lbk_csr* A,
+                                const float* x, float beta, float* y);
+lbk_status lbk_spmv_coo_f64(lbk_ctx, const lbk_coo* A, const double* x, double* y);
+lbk_status lbk_spmv_coo_f32(lbk_ctx, const lbk_coo* A, const float* x, float* y);
+lbk_status lbk_spmv_coo_adv_f64(lbk_ctx, double alpha, const lbk_coo* A,
+                                const double* x, double beta, double* y);
+lbk_status lbk_spmv_ell_f64(lbk_ctx, const lbk_ell* A, const double* x, double* y);
+lbk_status lbk_spmv_ell_f32(lbk_ctx, const lbk_ell* A, const float* x, float* y);
+lbk_status lbk_spmv_ell_adv_f64(lbk_ctx, double alpha, const lbk_ell* A,
+                                const double* x, double beta, double* y);
+lbk_status lbk_spmv_sellp_f64(lbk_ctx, const lbk_sellp* A, const double* x, double* y);
+lbk_status lbk_spmv_sellp_f32(lbk_ctx, const lbk_sellp* A, const float* x, float* y);
+lbk_status lbk_spmv_sellp_adv_f64(lbk_ctx, double alpha, const lbk_sellp* A,
+                                  const double* x, double beta, double* y);
+
+/* Load-balance plans (Ginkgo's "strategy" objects; the reference has none).
+ * CSR: nnz-balanced row tiles; tile_rows needs lbk_csr_plan_size() int32s.
+ * COO: row-aligned entry tiles. */
+lbk_status lbk_csr_plan_size(const lbk_csr* A, int32_t* ntiles_out);
+lbk_status lbk_csr_plan(lbk_ctx, const lbk_csr* A, int32_t* tile_rows_dev);
+lbk_status lbk_coo_plan_size(const lbk_coo* A, int32_t* ntiles_out);
+lbk_status lbk_coo_plan(lbk_ctx, const lbk_coo* A, int32_t* tile_starts_dev);
+
+/* ------------------------------------------------------------ BLAS-1 */
+/* kernels.hpp:79-91, api.cpp:69-110.  Reductions are deterministic (fixed
+ * two-stage tree), so repeated calls are bitwise reproducible. */
+lbk_status lbk_axpy_f64(lbk_ctx, int64_t n, double alpha, const double* x, double* y);
+lbk_status lbk_scal_f64(lbk_ctx, int64_t n, double alpha, double* x);
+lbk_status lbk_fill_f64(lbk_ctx, int64_t n, double value, double* x);
+lbk_status lbk_copy_f64(lbk_ctx, int64_t n, const double* x, double* y);
+/* result to HOST (synchronises) */
+lbk_status lbk_dot_f64(lbk_ctx, int64_t n, const double* x, const double* y, double* result);
+lbk_status lbk_nrm2_f64(lbk_ctx, int64_t n, const double* x, double* result);
+/* result to DEVICE memory (stream-ordered, no sync) */
+lbk_status lbk_dot_f64_dev(lbk_ctx, int64_t n, const double* x, const double* y, double* result_dev);
+
+/* ------------------------------------------------------- conversions */
+/* coo_to_csr (formats.cpp:132-155): row histogram + scan; col/vals are
+ * identical to the COO arrays (CSR inherits COO order), so only row_ptr is
+ * produced. */
+lbk_status lbk_coo_to_csr(lbk_ctx, const lbk_coo* A, int32_t* row_ptr_out);
+/* csr_to_coo (formats.cpp:158-179): expand row_ptr into row indices. */
+lbk_status lbk_csr_to_coo(lbk_ctx, const lbk_csr* A, int32_t* row_idx_out);
+/* coo_from_entries (formats.cpp:78-116): bounds check (FormatError),
+ * stable sort by (row, col), duplicates summed in input order, explicit
+ * zeros kept.  Inputs/outputs are device arrays of length n; *nnz_out
+ * (host) receives the canonical count.  Synchronises. */
+lbk_status lbk_coo_assemble_f64(lbk_ctx, int32_t nrows, int32_t ncols, int64_t n,
+                                const int32_t* rows, const int32_t* cols,
+                                const double* vals, int32_t* rows_out,
+                                int32_t* cols_out, double* vals_out,
+                                int64_t* nnz_out);
+/* ELL: width = max row length (synchronises). */
+lbk_status lbk_csr_ell_width(lbk_ctx, const lbk_csr* A, int32_t* width_out);
+lbk_status lbk_csr_to_ell(lbk_ctx, const lbk_csr* A, int32_t width, int64_t stride,
+                          int32_t* cols_out, void* vals_out);
+/* SELL-P: slice_lengths[nslices], slice_sets[nslices+1] (device), stored
+ * element count to host (synchronises); then the fill. */
+lbk_status lbk_csr_sellp_plan(lbk_ctx, const lbk_csr* A, int32_t slice_size,
+                              int32_t* slice_lengths_out, int32_t* slice_sets_out,
+                              int64_t* stored_out);
+lbk_status lbk_csr_to_sellp(lbk_ctx, const lbk_csr* A, int32_t slice_size,
+                            const int32_t* slice_sets, int32_t* cols_out,
+                            void* vals_out);
+/* validate(Csr/Coo) (formats.cpp:182-242): LBK_FORMAT_ERROR on violation. */
+lbk_status lbk_validate_csr(lbk_ctx, const lbk_csr* A);
+lbk_status lbk_validate_coo(lbk_ctx, const lbk_coo* A);
+
+/* ----------------------------------------------------------- solvers */
+/* SolverConfig / SolveResult (krylov.hpp:22-44).  kind: 0 = CG, 1 =
+ * BiCGSTAB (krylov.hpp:17; CGS/GMRES are out of scope this round).
+ * residual_mode 0 = reference semantics: true residual ||b - A x||/||b||
+ * recomputed every iteration (krylov.cpp:77-84, 145, 221); 1 = recurrence
+ * residual for the stopping test, with the true residual verified before
+ * convergence is declared (iteration continues if verification fails). */
+typedef struct lbk_solver_cfg {
+    int32_t kind;
+    int32_t max_iters;     /* default 1000 */
+    double rel_tol;        /* default 1e-10 */
+    int32_t fixed_iters;   /* <= 0: unset */
+    int32_t residual_mode; /* 0 true residual each iteration, 1 recurrence */
+} lbk_solver_cfg;
+
+typedef struct lbk_solve_result {
+    int32_t converged;
+    int32_t iterations;
+    double final_rel_residual;
+    double elapsed;          /* seconds, device-timed */
+    int64_t flop_count;      /* reference accounting, krylov.cpp:41-69 */
+    int32_t breakdown_iter;  /* >0 when LBK_BREAKDOWN is returned */
+    int32_t history_len;     /* iterations + 1 */
+} lbk_solve_result;
+
+/* solve(A, b, x, cfg) (krylov.hpp:53-56, krylov.cpp:446-512, 587-598).
+ * x is the initial guess on entry and the solution on exit (device).
+ * history (HOST, may be NULL) receives min(history_len, history_cap)
+ * entries.  Validation errors as solve_impl (krylov.cpp:449-472).
+ * Breakdown -> LBK_BREAKDOWN with result->breakdown_iter set. */
+lbk_status lbk_solve_csr(lbk_ctx, const lbk_csr* A, const double* b, double* x,
+                         const lbk_solver_cfg* cfg, lbk_solve_result* result,
+                         double* history, int32_t history_cap);
+lbk_status lbk_solve_coo(lbk_ctx, const lbk_coo* A, const double* b, double* x,
+                         const lbk_solver_cfg* cfg, lbk_solve_result* result,
+                         double* history, int32_t history_cap);
+
+/* ------------------------------------------------ synthetic inputs */
+/* Benchmark configurations; input synthesis, not
+ * part of the measured path.  kind 0 = 2D 5-pt (m x m), 1 = 3D 7-pt
+ * (m^3, upwind gamma), 2 = 3D 27-pt (m^3); rows r = (k*m + i)*m + j,
+ * ascending columns.  Device arrays sized by lbk_gen_stencil_nnz. */
+int64_t lbk_gen_stencil_nnz(int kind, int m);
+lbk_status lbk_gen_stencil_csr(lbk_ctx, int kind, int m, double gamma, int32_t* row_ptr,
+                               int32_t* cols, double* vals);
+/* seeded_values (reference src/bench/harness.cpp:90-99): mt19937_64(seed),
+ * uniform_real_distribution(-1,1), HOST output. */
+void lbk_gen_seeded_values(int64_t n, uint64_t seed, double* out);
+/* App. B power-law generator (HOST); handle -> fill -> free. */
+void* lbk_gen_powerlaw(int32_t n, uint64_t seed, int32_t max_len, int32_t window, int64_t* nnz);
+void lbk_gen_powerlaw_fill(void* h, int32_t* row_ptr, int32_t* cols, double* vals);
+void lbk_gen_powerlaw_free(void* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBK_H */

@@ -1,0 +1,239 @@
+// lbk_internal.cuh -- shared host/device plumbing of the B200 sparse backend.
+//
+// Host side: the context (device + stream + arena accounting + scratch), the
+// status/exception bridge behind the C ABI, and launch helpers.
+// Device side: mbarrier / 1-D TMA bulk-copy wrappers (sm_100a PTX), cache-
+// hinted loads, warp/block reductions and the deterministic two-stage
+// grid reduction used by every dot product.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "lbk.h"
+
+namespace lbk {
+
+// ------------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+    lbk_status status;
+    int iteration = -1;
+    Error(lbk_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] inline void fail(lbk_status s, const std::string& m) { throw Error(s, m); }
+
+#define LBK_CUDA(call)                                                          \
+    do {                                                                        \
+        cudaError_t e_ = (call);                                                \
+        if (e_ != cudaSuccess)                                                  \
+            ::lbk::fail(LBK_CUDA_ERROR, std::string(#call ": ") +               \
+                                            cudaGetErrorString(e_));            \
+    } while (0)
+
+#define LBK_LAUNCH_CHECK() LBK_CUDA(cudaGetLastError())
+
+// ----------------------------------------------------------------- context
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace lbk
+
+struct lbk_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int num_sms = 148;
+    size_t smem_optin = 0;
+    std::string err;
+    size_t arena_capacity = ~size_t{0};
+    size_t arena_used = 0;
+    // Scratch regions (device).  `scratch` holds per-call temporaries such
+    // as on-the-fly SpMV plans; `red` holds reduction partials + counters
+    // (counters are left zeroed by every reduction, see GridReduce).
+    lbk::DevBuf scratch;
+    lbk::DevBuf red;
+    double* host_pinned = nullptr;  // 64 doubles for synchronous readbacks
+};
+
+namespace lbk {
+
+// Ensure the context's scratch buffer holds `bytes`; returns device ptr.
+void* scratch(lbk_ctx ctx, size_t bytes);
+
+// Reduction workspace: `slots` partial doubles per block plus one counter.
+struct RedWs {
+    double* partials;     // [max_blocks * slots]
+    unsigned* counter;    // zero between uses
+    double* out;          // [slots] device result
+};
+RedWs red_ws(lbk_ctx ctx, int max_blocks, int slots);
+
+constexpr int kRedMaxBlocks = 4096;
+
+// --------------------------------------------------------- device helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile(
+        "mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "r"(bytes)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar)
+{
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra LAB_WAIT;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// L2 eviction policies for the bulk streams (matrix values / indices are
+// read exactly once per SpMV: evict-first keeps the gathered vector in L2).
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// 1-D TMA: global -> shared bulk copy completing on an mbarrier
+// (cp.async.bulk; src/dst 16-B aligned, size a multiple of 16).
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem,
+                                            uint32_t bytes, uint64_t* bar,
+                                            uint64_t policy)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::"
+        "cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ T ldg_nc(const T* p)
+{
+    return __ldg(p);
+}
+
+// Exact-rounding arithmetic helpers: products and sums are rounded
+// separately (no FMA contraction), which is what the FMA-free reference
+// build computes.
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = add_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide sum of NV doubles over the first `nthreads` threads (all of
+// which must call).  Result valid in thread 0.  Fixed order => deterministic.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], int tid, int nthreads,
+                                          double* sh /* >= 32*NV */)
+{
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+    const int warp = tid >> 5, lane = tid & 31, nw = (nthreads + 31) >> 5;
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) sh[warp * NV + i] = v[i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double t = lane < nw ? sh[lane * NV + i] : 0.0;
+            v[i] = warp_sum(t);
+        }
+    }
+}
+
+// Second stage of a deterministic grid reduction: called by every block
+// with its block total in thread 0.  The last block to arrive sums all
+// partials in block order and calls fin(totals) in thread 0.  Returns true
+// in the block that ran the finisher.
+template <int NV, class Fin>
+__device__ __forceinline__ bool grid_reduce_finish(const double (&v)[NV], RedWs ws,
+                                                   int tid, int nthreads, double* sh,
+                                                   Fin&& fin)
+{
+    __shared__ unsigned s_last;
+    if (tid == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) ws.partials[blockIdx.x * NV + i] = v[i];
+        __threadfence();
+        unsigned prev = atomicAdd(ws.counter, 1u);
+        s_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+    double acc[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    for (int b = tid; b < (int)gridDim.x; b += nthreads) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+            acc[i] = add_rn(acc[i], __ldcg(&ws.partials[b * NV + i]));
+    }
+    __syncthreads();
+    block_sum<NV>(acc, tid, nthreads, sh);
+    if (tid == 0) {
+        fin(acc);
+        *ws.counter = 0;
+    }
+    return true;
+}
+
+inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace lbk

@@ -1,0 +1,738 @@
+// solver.cu -- device-resident, fused CG and BiCGSTAB.
+//
+// Reference: src/solver/krylov.cpp (paths relative to /root/reference/proj)
+//   solve_impl      :446-512  validation, zero-b short-circuit, result
+//   run_cg          :119-161  CG with true-residual stop every iteration
+//   run_bicgstab    :164-230  BiCGSTAB, same stopping rule
+//   Workspace       :36-88    flop accounting (apply 2nnz; dot/norm/axpy 2n;
+//                             scal n) -- reproduced exactly
+//   check_breakdown :91-97    |v| < 1e-30 -> BreakdownError(iteration)
+//   machine_floor   :23       fixed-iteration freeze at rel <= 1e-13
+//
+// Every scalar of the recurrences lives in device memory (SolverState).
+// Each fused kernel ends in a deterministic grid reduction whose last block
+// ("finisher", one thread) advances the scalar recurrence, records the
+// residual history, detects breakdown / convergence / freeze and raises
+// `done`; every later kernel of the solve then exits immediately.  The host
+// only launches chunks of iterations and polls `done` once per chunk, so
+// there is no host round-trip per dot product (the reference synchronises
+// on every dot, api.cpp:95-104).
+//
+// Per-iteration kernels (reference semantics, residual_mode 0):
+//   CG        K1  q = A p            | <p,q>
+//             K2  x += a p, r -= a q  | <r,r>
+//             K3  t = b - A x         | <t,t>   + fused p = beta p + r
+//   BiCGSTAB  B2  v = A p            | <rt,v>
+//             B3  s = r - a v         | <s,s>
+//             B4  t = A s            | <t,t>, <t,s>
+//             B5  x += a p + w s; r = s - w t | <rt,r>
+//             B6  t = b - A x         | <t,t>   + fused next p update
+// residual_mode 1 (CG only) drops K3's SpMV: the stopping test uses the
+// recurrence residual sqrt(<r,r>)/||b||, and a true residual is computed
+// and must pass before convergence is declared.
+#include <chrono>
+#include <vector>
+
+#include "api_guard.h"
+#include "spmv_launch.cuh"
+
+namespace lbk {
+
+namespace {
+
+constexpr double kBreakdownEps = 1e-30;  // krylov.cpp:18
+constexpr double kMachineFloor = 1e-13;  // krylov.cpp:23
+
+enum : int { ST_RUNNING = 0, ST_CONVERGED = 1, ST_LIMIT = 2, ST_BREAKDOWN = 3, ST_FROZEN = 4 };
+
+struct SolverState {
+    int done;
+    int status;
+    int iter;
+    int breakdown_iter;
+    int breakdown_what;  // 0 <p,Ap>, 1 rho, 2 omega, 3 <rt,Ap>, 4 <t,t>
+    int hist_len;
+    int limit;
+    int fixed;
+    int verify_pending;  // residual_mode 1: true residual requested
+    int pad;
+    double tol, norm_b;
+    double rho, rho_next, alpha, beta, omega;
+    double s_rel;
+    double last_rel;
+    long long n, nnz;
+    long long flops;
+    double* hist;
+};
+
+__device__ __forceinline__ bool bd(double v) { return fabs(v) < kBreakdownEps; }
+
+__device__ void push_hist(SolverState* st, double rel)
+{
+    st->hist[st->hist_len] = rel;
+    st->hist_len += 1;
+    st->last_rel = rel;
+}
+
+__device__ void raise_breakdown(SolverState* st, int what, int iter)
+{
+    st->status = ST_BREAKDOWN;
+    st->breakdown_what = what;
+    st->breakdown_iter = iter;
+    st->done = 1;
+}
+
+// ---------------------------------------------------------- epilogues
+// Initial residual r = b - A x (krylov.cpp:108-116: apply, scal(-1),
+// axpy(1,b) == b - Ax exactly), copies to p (and rt), <r,r>.
+struct EpiInit {
+    static constexpr int NV = 1;
+    const double* __restrict__ b;
+    double* __restrict__ r;
+    double* __restrict__ p;
+    double* __restrict__ rt;  // may be null
+    SolverState* st;
+    int bicg;
+    __device__ bool skip() const { return false; }
+    __device__ void row(int i, double s, double* acc) const
+    {
+        const double v = add_rn(b[i], -s);
+        r[i] = v;
+        p[i] = v;
+        if (rt) rt[i] = v;
+        acc[0] = add_rn(acc[0], mul_rn(v, v));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        const double rr = tot[0];
+        const double rel = sqrt(rr) / st->norm_b;
+        st->hist_len = 0;
+        push_hist(st, rel);
+        const long long n = st->n;
+        st->flops += 2 * st->nnz + n + 2 * n + 2 * n;  // apply, scal, axpy, norm
+        if (!st->fixed && rel <= st->tol) {
+            st->status = ST_CONVERGED;
+            st->done = 1;
+            return;
+        }
+        if (!bicg) {
+            st->rho = rr;  // rho = dot(r, r)
+            st->flops += 2 * n;
+        } else {
+            // iteration 1 preamble (krylov.cpp:188, 198): rho = dot(rt, r)
+            // with rt == r, so it equals <r,r> bit for bit; no p update.
+            st->iter = 1;
+            st->flops += 2 * n;
+            st->rho = rr;
+            st->alpha = 1.0;
+            st->omega = 1.0;
+        }
+    }
+};
+
+// CG K1: q = A p, <p,q>
+struct EpiCgK1 {
+    static constexpr int NV = 1;
+    double* __restrict__ q;
+    const double* __restrict__ p;
+    SolverState* st;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void row(int i, double s, double* acc) const
+    {
+        q[i] = s;
+        acc[0] = add_rn(acc[0], mul_rn(p[i], s));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        const int iter = st->iter + 1;
+        st->iter = iter;
+        const double pq = tot[0];
+        st->flops += 2 * st->nnz + 2 * st->n;
+        if (bd(pq)) {
+            raise_breakdown(st, 0, iter);
+            return;
+        }
+        st->alpha = st->rho / pq;
+    }
+};
+
+// CG K3: true residual (+ fused p = beta p + r for the next iteration).
+struct EpiCgK3 {
+    static constexpr int NV = 1;
+    const double* __restrict__ b;
+    double* __restrict__ p;
+    const double* __restrict__ r;
+    SolverState* st;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void row(int i, double s, double* acc) const
+    {
+        const double t = add_rn(b[i], -s);
+        acc[0] = add_rn(acc[0], mul_rn(t, t));
+        const double beta = st->beta;
+        p[i] = add_rn(mul_rn(p[i], beta), r[i]);
+    }
+    __device__ void finish(const double* tot) const;
+};
+
+__device__ void cg_after_residual(SolverState* st, double rel)
+{
+    const long long n = st->n;
+    push_hist(st, rel);
+    if (!st->fixed && rel <= st->tol) {
+        st->status = ST_CONVERGED;
+        st->done = 1;
+        return;
+    }
+    if (st->fixed && rel <= kMachineFloor) {
+        st->status = ST_FROZEN;
+        st->done = 1;
+        return;
+    }
+    // rho_next = dot(r, r); check_breakdown(rho); beta; scal; axpy
+    st->flops += 2 * n + n + 2 * n;
+    if (bd(st->rho)) {
+        raise_breakdown(st, 1, st->iter);
+        return;
+    }
+    st->rho = st->rho_next;
+    if (st->iter >= st->limit) {
+        st->status = ST_LIMIT;
+        st->done = 1;
+    }
+}
+
+__device__ void EpiCgK3::finish(const double* tot) const
+{
+    st->flops += 2 * st->nnz + st->n + 2 * st->n + 2 * st->n;  // true_residual
+    cg_after_residual(st, sqrt(tot[0]) / st->norm_b);
+}
+
+// residual_mode 1: stand-alone true residual check (no p update).
+struct EpiTrueRes {
+    static constexpr int NV = 1;
+    const double* __restrict__ b;
+    SolverState* st;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0 || !st->verify_pending; }
+    __device__ void row(int i, double s, double* acc) const
+    {
+        const double t = add_rn(b[i], -s);
+        acc[0] = add_rn(acc[0], mul_rn(t, t));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        st->flops += 2 * st->nnz + st->n + 2 * st->n + 2 * st->n;
+        const double rel = sqrt(tot[0]) / st->norm_b;
+        st->verify_pending = 0;
+        // replace the recurrence estimate of this iteration by the truth
+        st->hist[st->hist_len - 1] = rel;
+        st->last_rel = rel;
+        if (rel <= st->tol) {
+            st->status = ST_CONVERGED;
+            st->done = 1;
+        } else if (st->iter >= st->limit) {
+            st->status = ST_LIMIT;
+            st->done = 1;
+        } else {
+            // verification failed: continue the recurrence (rho update that
+            // OpCgK2 deferred)
+            st->flops += 5 * st->n;
+            if (bd(st->rho)) {
+                raise_breakdown(st, 1, st->iter);
+                return;
+            }
+            st->rho = st->rho_next;
+        }
+    }
+};
+
+// BiCGSTAB B2: v = A p, <rt,v>
+struct EpiBiB2 {
+    static constexpr int NV = 1;
+    double* __restrict__ v;
+    const double* __restrict__ rt;
+    SolverState* st;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void row(int i, double s, double* acc) const
+    {
+        v[i] = s;
+        acc[0] = add_rn(acc[0], mul_rn(rt[i], s));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        st->flops += 2 * st->nnz + 2 * st->n;
+        const double rtv = tot[0];
+        if (bd(rtv)) {
+            raise_breakdown(st, 3, st->iter);
+            return;
+        }
+        st->alpha = st->rho / rtv;
+    }
+};
+
+// BiCGSTAB B4: t = A s, <t,t>, <t,s>
+struct EpiBiB4 {
+    static constexpr int NV = 2;
+    double* __restrict__ t;
+    const double* __restrict__ s;
+    SolverState* st;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void row(int i, double sum, double* acc) const
+    {
+        t[i] = sum;
+        acc[0] = add_rn(acc[0], mul_rn(sum, sum));
+        acc[1] = add_rn(acc[1], mul_rn(sum, s[i]));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        st->flops += 2 * st->nnz + 2 * st->n;
+        const double tt = tot[0];
+        if (bd(tt)) {
+            if (st->s_rel > kMachineFloor) {
+                raise_breakdown(st, 4, st->iter);
+                return;
+            }
+            st->omega = 0.0;  // exact half-step convergence
+        } else {
+            st->flops += 2 * st->n;
+            st->omega = tot[1] / tt;
+        }
+    }
+};
+
+// BiCGSTAB B6: true residual + fused p = (p - w v) beta + r for iter+1.
+struct EpiBiB6 {
+    static constexpr int NV = 1;
+    const double* __restrict__ b;
+    double* __restrict__ p;
+    const double* __restrict__ v;
+    const double* __restrict__ r;
+    SolverState* st;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void row(int i, double s, double* acc) const
+    {
+        const double t = add_rn(b[i], -s);
+        acc[0] = add_rn(acc[0], mul_rn(t, t));
+        const double beta = st->beta, omega = st->omega;
+        p[i] = add_rn(mul_rn(add_rn(p[i], mul_rn(-omega, v[i])), beta), r[i]);
+    }
+    __device__ void finish(const double* tot) const
+    {
+        const long long n = st->n;
+        st->flops += 2 * st->nnz + n + 2 * n + 2 * n;
+        const double rel = sqrt(tot[0]) / st->norm_b;
+        push_hist(st, rel);
+        if (!st->fixed && rel <= st->tol) {
+            st->status = ST_CONVERGED;
+            st->done = 1;
+            return;
+        }
+        if (st->fixed && rel <= kMachineFloor) {
+            st->status = ST_FROZEN;
+            st->done = 1;
+            return;
+        }
+        if (st->iter >= st->limit) {
+            st->status = ST_LIMIT;
+            st->done = 1;
+            return;
+        }
+        // start of iteration iter+1 (krylov.cpp:188-198): dot(rt, r) was
+        // reduced in B5; checks on rho and omega; p update (done in row()).
+        const int next = st->iter + 1;
+        st->iter = next;
+        st->flops += 2 * n;
+        if (bd(st->rho)) {
+            raise_breakdown(st, 1, next);
+            return;
+        }
+        if (bd(st->omega)) {
+            raise_breakdown(st, 2, next);
+            return;
+        }
+        st->flops += 2 * n + n + 2 * n;
+        st->rho = st->rho_next;
+    }
+};
+
+// ------------------------------------------------ element-wise steps
+template <class Op>
+__global__ void __launch_bounds__(256) vec_kernel(long long n, Op op, RedWs ws)
+{
+    constexpr int NV = Op::NV;
+    __shared__ double sh[32 * NV];
+    if (op.skip()) return;
+    double acc[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    op.prologue();
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        op.elem(i, acc);
+    block_sum<NV>(acc, threadIdx.x, blockDim.x, sh);
+    grid_reduce_finish<NV>(acc, ws, threadIdx.x, blockDim.x, sh,
+                           [&](const double* tot) { op.finish(tot); });
+}
+
+// CG K2: x += alpha p; r -= alpha q; <r,r>; beta = <r,r>/rho (for K3).
+struct OpCgK2 {
+    static constexpr int NV = 1;
+    double* __restrict__ x;
+    double* __restrict__ r;
+    const double* __restrict__ p;
+    const double* __restrict__ q;
+    SolverState* st;
+    int recurrence;
+    double alpha;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prologue() { alpha = st->alpha; }
+    __device__ void elem(long long i, double* acc) const
+    {
+        x[i] = add_rn(x[i], mul_rn(alpha, p[i]));
+        const double rn = add_rn(r[i], mul_rn(-alpha, q[i]));
+        r[i] = rn;
+        acc[0] = add_rn(acc[0], mul_rn(rn, rn));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        st->flops += 4 * st->n;
+        st->rho_next = tot[0];
+        st->beta = tot[0] / st->rho;
+        if (recurrence) {
+            // stopping test on the recurrence residual; a true residual
+            // must confirm convergence (EpiTrueRes), else iteration goes on
+            const double rel = sqrt(tot[0]) / st->norm_b;
+            const long long n = st->n;
+            st->hist[st->hist_len] = rel;
+            st->hist_len += 1;
+            st->last_rel = rel;
+            if (rel <= st->tol || st->iter >= st->limit) {
+                st->verify_pending = 1;
+                return;
+            }
+            st->flops += 2 * n + n + 2 * n;
+            if (bd(st->rho)) {
+                raise_breakdown(st, 1, st->iter);
+                return;
+            }
+            st->rho = st->rho_next;
+        }
+    }
+};
+
+// residual_mode 1: p = beta p + r (skipped while a verification is pending)
+struct OpCgP {
+    static constexpr int NV = 1;
+    double* __restrict__ p;
+    const double* __restrict__ r;
+    SolverState* st;
+    double beta;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prologue() { beta = st->beta; }
+    __device__ void elem(long long i, double*) const { p[i] = add_rn(mul_rn(p[i], beta), r[i]); }
+    __device__ void finish(const double*) const {}
+};
+
+// BiCGSTAB B3: s = r - alpha v; <s,s>
+struct OpBiB3 {
+    static constexpr int NV = 1;
+    double* __restrict__ s;
+    const double* __restrict__ r;
+    const double* __restrict__ v;
+    SolverState* st;
+    double alpha;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prologue() { alpha = st->alpha; }
+    __device__ void elem(long long i, double* acc) const
+    {
+        const double sv = add_rn(r[i], mul_rn(-alpha, v[i]));
+        s[i] = sv;
+        acc[0] = add_rn(acc[0], mul_rn(sv, sv));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        st->flops += 4 * st->n;  // axpy + norm
+        st->s_rel = sqrt(tot[0]) / st->norm_b;
+    }
+};
+
+// BiCGSTAB B5: x += alpha p; x += omega s; r = s - omega t; <rt, r>
+struct OpBiB5 {
+    static constexpr int NV = 1;
+    double* __restrict__ x;
+    double* __restrict__ r;
+    const double* __restrict__ p;
+    const double* __restrict__ s;
+    const double* __restrict__ t;
+    const double* __restrict__ rt;
+    SolverState* st;
+    double alpha, omega;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prologue()
+    {
+        alpha = st->alpha;
+        omega = st->omega;
+    }
+    __device__ void elem(long long i, double* acc) const
+    {
+        const double si = s[i];
+        x[i] = add_rn(add_rn(x[i], mul_rn(alpha, p[i])), mul_rn(omega, si));
+        const double rn = add_rn(si, mul_rn(-omega, t[i]));
+        r[i] = rn;
+        acc[0] = add_rn(acc[0], mul_rn(rt[i], rn));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        st->flops += 6 * st->n;
+        st->rho_next = tot[0];
+        // beta for the p update fused into B6 (checked there)
+        st->beta = (tot[0] / st->rho) * (st->alpha / st->omega);
+    }
+};
+
+// -------------------------------------------------------- operators
+struct CsrOp {
+    CsrView<double> A;
+    template <class Epi>
+    void apply(lbk_ctx ctx, const double* x, const Epi& e, RedWs ws) const
+    {
+        launch_csr<double>(ctx, A, x, e, ws);
+    }
+};
+
+struct CooOp {
+    CooView<double> A;
+    template <class Epi>
+    void apply(lbk_ctx ctx, const double* x, const Epi& e, RedWs ws) const
+    {
+        launch_coo<double>(ctx, A, x, e, ws);
+    }
+};
+
+template <class Op>
+void launch_vec(lbk_ctx ctx, long long n, const Op& op, RedWs ws)
+{
+    auto k = vec_kernel<Op>;
+    static int bps = blocks_per_sm(k, 256, 0);
+    long long want = (n + 255) / 256;
+    long long cap = static_cast<long long>(ctx->num_sms) * bps;
+    if (cap > kRedMaxBlocks) cap = kRedMaxBlocks;
+    int grid = static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap);
+    k<<<grid, 256, 0, ctx->stream>>>(n, op, ws);
+    LBK_LAUNCH_CHECK();
+}
+
+struct DevBufs {
+    std::vector<void*> ptrs;
+    cudaStream_t s;
+    explicit DevBufs(cudaStream_t st) : s(st) {}
+    template <typename T>
+    T* get(size_t count)
+    {
+        void* p = nullptr;
+        LBK_CUDA(cudaMallocAsync(&p, count * sizeof(T) + 16, s));
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    ~DevBufs()
+    {
+        for (auto* p : ptrs) cudaFreeAsync(p, s);
+    }
+};
+
+const char* breakdown_what(int w)
+{
+    switch (w) {
+    case 0: return "division by vanishing <p, Ap>";
+    case 1: return "division by vanishing rho";
+    case 2: return "division by vanishing omega";
+    case 3: return "division by vanishing <rt, Ap>";
+    default: return "division by vanishing <t, t>";
+    }
+}
+
+template <class Op>
+void solve_impl(lbk_ctx ctx, const Op& op, long long n, long long nnz, const double* b, double* x,
+                const lbk_solver_cfg* cfg, lbk_solve_result* res, double* history, int hist_cap)
+{
+    // krylov.cpp:449-472 validation
+    need(cfg != nullptr && res != nullptr, LBK_USAGE_ERROR, "solve: null config/result");
+    need(cfg->max_iters >= 1, LBK_CONFIGURATION_ERROR, "max_iters must be positive");
+    need(cfg->rel_tol > 0.0, LBK_CONFIGURATION_ERROR, "rel_tol must be positive");
+    need(cfg->kind == 0 || cfg->kind == 1, LBK_CONFIGURATION_ERROR,
+         "solver kind must be 0 (cg) or 1 (bicgstab)");
+    need(cfg->residual_mode == 0 || (cfg->residual_mode == 1 && cfg->kind == 0),
+         LBK_CONFIGURATION_ERROR, "residual_mode 1 is implemented for CG only");
+    need(cfg->residual_mode == 0 || cfg->fixed_iters <= 0, LBK_CONFIGURATION_ERROR,
+         "residual_mode 1 cannot be combined with fixed_iters");
+    std::memset(res, 0, sizeof(*res));
+
+    const bool fixed = cfg->fixed_iters > 0;
+    const int limit = fixed ? cfg->fixed_iters : cfg->max_iters;
+    const bool bicg = cfg->kind == 1;
+    const bool recurrence = cfg->residual_mode == 1;
+
+    cudaEvent_t ev0, ev1;
+    LBK_CUDA(cudaEventCreate(&ev0));
+    LBK_CUDA(cudaEventCreate(&ev1));
+    LBK_CUDA(cudaEventRecord(ev0, ctx->stream));
+
+    DevBufs bufs(ctx->stream);
+    auto* st = bufs.get<SolverState>(1);
+    auto* hist = bufs.get<double>(size_t(limit) + 2);
+    // norm_b (krylov.cpp:478) -- host value needed for the zero-b rule
+    double norm_b = 0.0;
+    if (lbk_nrm2_f64(ctx, n, b, &norm_b) != LBK_OK) fail(LBK_CUDA_ERROR, ctx->err);
+    RedWs ws = red_ws(ctx, kRedMaxBlocks, 2);
+    SolverState h{};
+    h.limit = limit;
+    h.fixed = fixed ? 1 : 0;
+    h.tol = cfg->rel_tol;
+    h.norm_b = norm_b;
+    h.n = n;
+    h.nnz = nnz;
+    h.flops = 2 * n;
+    h.hist = hist;
+    if (norm_b == 0.0) {
+        // krylov.cpp:479-482: x = 0, converged, history [0]
+        LBK_CUDA(cudaMemsetAsync(x, 0, size_t(n) * sizeof(double), ctx->stream));
+        LBK_CUDA(cudaEventRecord(ev1, ctx->stream));
+        LBK_CUDA(cudaEventSynchronize(ev1));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        res->converged = 1;
+        res->iterations = 0;
+        res->final_rel_residual = 0.0;
+        res->history_len = 1;
+        res->flop_count = 2 * n;
+        res->elapsed = ms * 1e-3;
+        if (history && hist_cap > 0) history[0] = 0.0;
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+        return;
+    }
+    LBK_CUDA(cudaMemcpyAsync(st, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+
+    double* r = bufs.get<double>(n);
+    double* p = bufs.get<double>(n);
+    double* q = bufs.get<double>(n);  // CG q / BiCGSTAB v
+    double* rt = bicg ? bufs.get<double>(n) : nullptr;
+    double* s = bicg ? bufs.get<double>(n) : nullptr;
+    double* t = bicg ? bufs.get<double>(n) : nullptr;
+
+    op.apply(ctx, x, EpiInit{b, r, p, rt, st, bicg ? 1 : 0}, ws);
+
+    // chunked launch loop; `done` is polled once per chunk
+    int* done_host = reinterpret_cast<int*>(ctx->host_pinned);
+    const int chunk = 16;
+    int launched = 0;
+    for (;;) {
+        for (int c = 0; c < chunk && launched < limit; ++c, ++launched) {
+            if (!bicg) {
+                op.apply(ctx, p, EpiCgK1{q, p, st}, ws);
+                launch_vec(ctx, n, OpCgK2{x, r, p, q, st, recurrence ? 1 : 0, 0.0}, ws);
+                if (!recurrence) {
+                    op.apply(ctx, x, EpiCgK3{b, p, r, st}, ws);
+                } else {
+                    op.apply(ctx, x, EpiTrueRes{b, st}, ws);
+                    launch_vec(ctx, n, OpCgP{p, r, st, 0.0}, ws);
+                }
+            } else {
+                op.apply(ctx, p, EpiBiB2{q, rt, st}, ws);
+                launch_vec(ctx, n, OpBiB3{s, r, q, st, 0.0}, ws);
+                op.apply(ctx, s, EpiBiB4{t, s, st}, ws);
+                launch_vec(ctx, n, OpBiB5{x, r, p, s, t, rt, st, 0.0, 0.0}, ws);
+                op.apply(ctx, x, EpiBiB6{b, p, q, r, st}, ws);
+            }
+        }
+        LBK_CUDA(cudaMemcpyAsync(done_host, &st->done, sizeof(int), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        LBK_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (*done_host || launched >= limit) break;
+    }
+    LBK_CUDA(cudaEventRecord(ev1, ctx->stream));
+    LBK_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    LBK_CUDA(cudaStreamSynchronize(ctx->stream));
+    float ms = 0;
+    LBK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+
+    std::vector<double> hv(static_cast<size_t>(h.hist_len));
+    if (h.hist_len)
+        LBK_CUDA(cudaMemcpy(hv.data(), hist, hv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    if (h.status == ST_FROZEN) {
+        // krylov.cpp:135-137: frozen iterations repeat the last entry
+        while (static_cast<int>(hv.size()) < limit + 1) hv.push_back(hv.back());
+    }
+    res->iterations = static_cast<int>(hv.size()) - 1;
+    res->history_len = static_cast<int>(hv.size());
+    res->final_rel_residual = hv.back();
+    res->converged = res->final_rel_residual <= cfg->rel_tol ? 1 : 0;
+    res->flop_count = h.flops;
+    res->elapsed = ms * 1e-3;
+    if (history) {
+        const int m = res->history_len < hist_cap ? res->history_len : hist_cap;
+        for (int i = 0; i < m; ++i) history[i] = hv[i];
+    }
+    if (h.status == ST_BREAKDOWN) {
+        res->breakdown_iter = h.breakdown_iter;
+        Error e(LBK_BREAKDOWN, std::string(breakdown_what(h.breakdown_what)) + " at iteration " +
+                                   std::to_string(h.breakdown_iter));
+        throw e;
+    }
+}
+
+}  // namespace
+}  // namespace lbk
+
+using namespace lbk;
+
+extern "C" {
+
+lbk_status lbk_solve_csr(lbk_ctx ctx, const lbk_csr* A, const double* b, double* x,
+                         const lbk_solver_cfg* cfg, lbk_solve_result* result, double* history,
+                         int32_t history_cap)
+{
+    if (!ctx || !A) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        need(A->dtype == LBK_F64, LBK_TYPE_ERROR, "solve: FP64 matrices only");
+        need(A->nrows == A->ncols, LBK_SHAPE_ERROR,
+             "solve requires a square matrix, got " + std::to_string(A->nrows) + "x" +
+                 std::to_string(A->ncols));
+        CsrOp op{CsrView<double>{A->nrows, A->ncols, A->nnz, A->row_ptr, A->col_idx,
+                                 static_cast<const double*>(A->vals), A->tile_rows, A->ntiles}};
+        if (!op.A.tile_rows && A->nrows > 0 && aligned16(A->vals) && aligned16(A->col_idx)) {
+            // build the plan once for the whole solve
+            op.A.ntiles = csr_ntiles(A->nnz);
+            int* plan = static_cast<int*>(scratch(ctx, size_t(op.A.ntiles + 1) * sizeof(int)));
+            csr_plan_launch(ctx, A->row_ptr, A->nrows, A->nnz, plan);
+            op.A.tile_rows = plan;
+        }
+        solve_impl(ctx, op, A->nrows, A->nnz, b, x, cfg, result, history, history_cap);
+    });
+}
+
+lbk_status lbk_solve_coo(lbk_ctx ctx, const lbk_coo* A, const double* b, double* x,
+                         const lbk_solver_cfg* cfg, lbk_solve_result* result, double* history,
+                         int32_t history_cap)
+{
+    if (!ctx || !A) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        need(A->dtype == LBK_F64, LBK_TYPE_ERROR, "solve: FP64 matrices only");
+        need(A->nrows == A->ncols, LBK_SHAPE_ERROR,
+             "solve requires a square matrix, got " + std::to_string(A->nrows) + "x" +
+                 std::to_string(A->ncols));
+        need(A->nnz > 0, LBK_USAGE_ERROR, "solve: COO matrix without entries");
+        CooOp op{CooView<double>{A->nrows, A->ncols, A->nnz, A->row_idx, A->col_idx,
+                                 static_cast<const double*>(A->vals), A->tile_starts, A->ntiles}};
+        if (!op.A.tile_starts) {
+            op.A.ntiles = coo_ntiles(A->nnz);
+            int* plan = static_cast<int*>(scratch(ctx, size_t(op.A.ntiles + 1) * sizeof(int)));
+            coo_plan_launch(ctx, A->row_idx, A->nnz, plan);
+            op.A.tile_starts = plan;
+        }
+        solve_impl(ctx, op, A->nrows, A->nnz, b, x, cfg, result, history, history_cap);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,178 @@
+// spmv_launch.cuh -- host-side launchers for the SpMV kernels (plans, grid
+// sizing, alignment-driven kernel choice).  Shared by the SpMV entry points
+// (spmv.cu) and the fused solver steps (solver.cu).
+#pragma once
+
+#include <cstdlib>
+#include <cstring>
+
+#include "api_guard.h"
+#include "spmv_kernels.cuh"
+
+namespace lbk {
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline int csr_ntiles(long long nnz)
+{
+    long long t = (nnz + CsrCfg::kTile - 1) / CsrCfg::kTile;
+    return static_cast<int>(t < 1 ? 1 : t);
+}
+
+inline int coo_ntiles(long long nnz)
+{
+    long long t = (nnz + CooCfg::kTile - 1) / CooCfg::kTile;
+    return static_cast<int>(t < 1 ? 1 : t);
+}
+
+void csr_plan_launch(lbk_ctx ctx, const int* row_ptr, int nrows, long long nnz, int* tile_rows);
+void coo_plan_launch(lbk_ctx ctx, const int* rows, long long nnz, int* tile_starts);
+
+// Forces the warp-per-row CSR kernel (diagnostics / A-B comparison).
+inline bool csr_force_warp()
+{
+    static int v = [] {
+        const char* e = std::getenv("LBK_CSR_ALGO");
+        return (e && std::strcmp(e, "warp") == 0) ? 1 : 0;
+    }();
+    return v != 0;
+}
+
+// Warp-per-row CSR straight from global memory: the fallback for arrays
+// that are not 16-B aligned (TMA bulk copies need it).
+template <typename T, class Epi>
+__global__ void __launch_bounds__(256)
+    csr_warp_kernel(CsrView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
+{
+    constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
+    __shared__ double red_sh[32 * NV];
+    if (epi.skip()) return;
+    double acc[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    const int lane = threadIdx.x & 31;
+    const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long rr = w0; rr < A.nrows; rr += nw) {
+        const int r = static_cast<int>(rr);
+        const int rs = __ldg(A.row_ptr + r), re = __ldg(A.row_ptr + r + 1);
+        T part = T(0);
+        if (re - rs <= 32) {
+            // short row: lane k holds product k, lane 0 sums them in order
+            // (bit-identical to the sequential reference)
+            T p = T(0);
+            if (rs + lane < re) p = mul_rn(__ldg(A.vals + rs + lane), ldg_nc(x + __ldg(A.cols + rs + lane)));
+            T sum = T(0);
+            for (int k = 0; k < re - rs; ++k) sum = add_rn(sum, __shfl_sync(0xffffffffu, p, k));
+            part = sum;
+        } else {
+            for (int k = rs + lane; k < re; k += 32)
+                part = add_rn(part, mul_rn(__ldg(A.vals + k), ldg_nc(x + __ldg(A.cols + k))));
+            part = warp_sum(part);
+        }
+        if (lane == 0) epi.row(r, part, acc);
+    }
+    if constexpr (Epi::NV > 0) {
+        block_sum<NV>(acc, threadIdx.x, blockDim.x, red_sh);
+        grid_reduce_finish<NV>(acc, ws, threadIdx.x, blockDim.x, red_sh,
+                               [&](const double* tot) { epi.finish(tot); });
+    }
+}
+
+template <class K>
+int blocks_per_sm(K kernel, int threads, size_t smem)
+{
+    int b = 0;
+    LBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem));
+    return b < 1 ? 1 : b;
+}
+
+template <typename T, class Epi>
+void launch_csr(lbk_ctx ctx, CsrView<T> A, const T* x, const Epi& epi, RedWs ws)
+{
+    constexpr int NCW = CsrCfg::kConsumerWarps, CAP = CsrCfg::kCap, ST = CsrCfg::kStages;
+    const bool tma_ok = aligned16(A.vals) && aligned16(A.cols) && !csr_force_warp();
+    if (!tma_ok) {
+        auto k = csr_warp_kernel<T, Epi>;
+        static int bps = blocks_per_sm(k, 256, 0);
+        long long want = (static_cast<long long>(A.nrows) * 32 + 255) / 256;
+        long long cap = static_cast<long long>(ctx->num_sms) * bps;
+        int grid = static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap);
+        if (Epi::NV > 0 && grid > kRedMaxBlocks) grid = kRedMaxBlocks;
+        k<<<grid, 256, 0, ctx->stream>>>(A, x, epi, ws);
+        LBK_LAUNCH_CHECK();
+        return;
+    }
+    if (!A.tile_rows) {
+        A.ntiles = csr_ntiles(A.nnz);
+        int* plan = static_cast<int*>(scratch(ctx, size_t(A.ntiles + 1) * sizeof(int)));
+        csr_plan_launch(ctx, A.row_ptr, A.nrows, A.nnz, plan);
+        A.tile_rows = plan;
+    }
+    auto k = csr_staged_kernel<T, Epi, NCW, CAP, ST>;
+    constexpr size_t smem = csr_smem_bytes<T, CAP, ST>();
+    static bool attr = [&] {
+        LBK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        return true;
+    }();
+    (void)attr;
+    static int bps = blocks_per_sm(k, (NCW + 1) * 32, smem);
+    long long cap = static_cast<long long>(ctx->num_sms) * bps;
+    int grid = static_cast<int>(A.ntiles < cap ? A.ntiles : cap);
+    k<<<grid, (NCW + 1) * 32, smem, ctx->stream>>>(A, x, epi, ws);
+    LBK_LAUNCH_CHECK();
+}
+
+template <typename T, class Epi>
+void launch_coo(lbk_ctx ctx, CooView<T> A, const T* x, const Epi& epi, RedWs ws)
+{
+    constexpr int NCW = CooCfg::kConsumerWarps, CAP = CooCfg::kCap, ST = CooCfg::kStages;
+    need(aligned16(A.vals) && aligned16(A.cols) && aligned16(A.rows), LBK_USAGE_ERROR,
+         "COO arrays must be 16-byte aligned");
+    if (!A.tile_starts) {
+        A.ntiles = coo_ntiles(A.nnz);
+        int* plan = static_cast<int*>(scratch(ctx, size_t(A.ntiles + 1) * sizeof(int)));
+        coo_plan_launch(ctx, A.rows, A.nnz, plan);
+        A.tile_starts = plan;
+    }
+    auto k = coo_staged_kernel<T, Epi, NCW, CAP, ST>;
+    constexpr size_t smem = coo_smem_bytes<T, CAP, ST>();
+    static bool attr = [&] {
+        LBK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        return true;
+    }();
+    (void)attr;
+    static int bps = blocks_per_sm(k, (NCW + 1) * 32, smem);
+    long long cap = static_cast<long long>(ctx->num_sms) * bps;
+    int grid = static_cast<int>(A.ntiles < cap ? A.ntiles : cap);
+    k<<<grid, (NCW + 1) * 32, smem, ctx->stream>>>(A, x, epi, ws);
+    LBK_LAUNCH_CHECK();
+}
+
+// ELL (is_ell) or SELL-P over the sliced column-major layout.
+template <typename T, class Epi, bool IS_ELL>
+void launch_sliced(lbk_ctx ctx, int nrows, int S, const int* slice_sets, int width,
+                   long long ell_stride, const int* cols, const T* vals, const T* x,
+                   const Epi& epi, RedWs ws)
+{
+    const int pitch = IS_ELL ? static_cast<int>(ell_stride) : S;
+    const bool quad_ok = aligned16(cols) && aligned16(vals) && pitch % 4 == 0 &&
+                         (!IS_ELL || ell_stride >= ((static_cast<long long>(nrows) + 3) & ~3LL));
+    const long long units = quad_ok ? (static_cast<long long>(nrows) + 3) / 4 : nrows;
+    if (quad_ok) {
+        auto k = sliced_quad_kernel<T, Epi, IS_ELL>;
+        static int bps = blocks_per_sm(k, 256, 0);
+        long long want = (units + 255) / 256, cap = static_cast<long long>(ctx->num_sms) * bps;
+        int grid = static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap);
+        k<<<grid, 256, 0, ctx->stream>>>(nrows, pitch, slice_sets, width, cols, vals, x, epi, ws);
+    } else {
+        auto k = sliced_row_kernel<T, Epi, IS_ELL>;
+        static int bps = blocks_per_sm(k, 256, 0);
+        long long want = (units + 255) / 256, cap = static_cast<long long>(ctx->num_sms) * bps;
+        int grid = static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap);
+        k<<<grid, 256, 0, ctx->stream>>>(nrows, pitch, slice_sets, width, cols, vals, x, epi, ws);
+    }
+    LBK_LAUNCH_CHECK();
+}
+
+}  // namespace lbk
