@@ -89,6 +89,10 @@ def ref_available() -> bool:
     return os.path.exists(REF_SO)
 
 
+def ref_buildable() -> bool:
+    return os.path.isdir(os.environ.get("LARCH_REF_DIR", "/root/reference/proj"))
+
+
 def ref():
     global _ref
     if _ref is None:

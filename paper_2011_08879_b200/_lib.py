@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblbk.so")
+# LBK_LIB overrides the path (A/B timing of build variants); default in-tree.
+LIB_PATH = os.environ.get("LBK_LIB") or os.path.join(HERE, "liblbk.so")
 
 # ----------------------------------------------------------------- status
 OK = 0

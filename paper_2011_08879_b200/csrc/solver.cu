@@ -703,7 +703,7 @@ lbk_status lbk_solve_csr(lbk_ctx ctx, const lbk_csr* A, const double* b, double*
                                  static_cast<const double*>(A->vals), A->tile_rows, A->ntiles}};
         if (!op.A.tile_rows && A->nrows > 0 && aligned16(A->vals) && aligned16(A->col_idx)) {
             // build the plan once for the whole solve
-            op.A.ntiles = csr_ntiles(A->nnz);
+            op.A.ntiles = csr_ntiles(A->nnz, A->nrows);
             int* plan = static_cast<int*>(scratch(ctx, size_t(op.A.ntiles + 1) * sizeof(int)));
             csr_plan_launch(ctx, A->row_ptr, A->nrows, A->nnz, plan);
             op.A.tile_rows = plan;
@@ -726,9 +726,9 @@ lbk_status lbk_solve_coo(lbk_ctx ctx, const lbk_coo* A, const double* b, double*
         CooOp op{CooView<double>{A->nrows, A->ncols, A->nnz, A->row_idx, A->col_idx,
                                  static_cast<const double*>(A->vals), A->tile_starts, A->ntiles}};
         if (!op.A.tile_starts) {
-            op.A.ntiles = coo_ntiles(A->nnz);
+            op.A.ntiles = coo_ntiles(A->nnz, A->nrows);
             int* plan = static_cast<int*>(scratch(ctx, size_t(op.A.ntiles + 1) * sizeof(int)));
-            coo_plan_launch(ctx, A->row_idx, A->nnz, plan);
+            coo_plan_launch(ctx, A->row_idx, A->nrows, A->nnz, plan);
             op.A.tile_starts = plan;
         }
         solve_impl(ctx, op, A->nrows, A->nnz, b, x, cfg, result, history, history_cap);

@@ -44,17 +44,17 @@ __global__ void coo_plan_kernel(const int* __restrict__ rows, long long nnz, int
 
 void csr_plan_launch(lbk_ctx ctx, const int* row_ptr, int nrows, long long nnz, int* tile_rows)
 {
-    const int nt = csr_ntiles(nnz);
-    csr_plan_kernel<<<ceil_div(nt + 1, 256), 256, 0, ctx->stream>>>(row_ptr, nrows, nt,
-                                                                    CsrCfg::kTile, tile_rows);
+    const int nt = csr_ntiles(nnz, nrows);
+    csr_plan_kernel<<<ceil_div(nt + 1, 256), 256, 0, ctx->stream>>>(
+        row_ptr, nrows, nt, stream_tile_nnz(nnz, nrows), tile_rows);
     LBK_LAUNCH_CHECK();
 }
 
-void coo_plan_launch(lbk_ctx ctx, const int* rows, long long nnz, int* tile_starts)
+void coo_plan_launch(lbk_ctx ctx, const int* rows, int nrows, long long nnz, int* tile_starts)
 {
-    const int nt = coo_ntiles(nnz);
-    coo_plan_kernel<<<ceil_div(nt + 1, 256), 256, 0, ctx->stream>>>(rows, nnz, nt,
-                                                                    CooCfg::kTile, tile_starts);
+    const int nt = coo_ntiles(nnz, nrows);
+    coo_plan_kernel<<<ceil_div(nt + 1, 256), 256, 0, ctx->stream>>>(
+        rows, nnz, nt, stream_tile_nnz(nnz, nrows), tile_starts);
     LBK_LAUNCH_CHECK();
 }
 
@@ -79,7 +79,7 @@ CsrView<T> csr_view(const lbk_csr* A, lbk_dtype want)
     CsrView<T> v{A->nrows, A->ncols, A->nnz, A->row_ptr, A->col_idx,
                  static_cast<const T*>(A->vals), A->tile_rows, A->ntiles};
     if (v.tile_rows)
-        need(v.ntiles == csr_ntiles(v.nnz), LBK_USAGE_ERROR,
+        need(v.ntiles == csr_ntiles(v.nnz, v.nrows), LBK_USAGE_ERROR,
              "spmv_csr: stale plan (ntiles does not match lbk_csr_plan_size)");
     return v;
 }
@@ -92,7 +92,7 @@ CooView<T> coo_view(const lbk_coo* A, lbk_dtype want)
     CooView<T> v{A->nrows, A->ncols, A->nnz, A->row_idx, A->col_idx,
                  static_cast<const T*>(A->vals), A->tile_starts, A->ntiles};
     if (v.tile_starts)
-        need(v.ntiles == coo_ntiles(v.nnz), LBK_USAGE_ERROR,
+        need(v.ntiles == coo_ntiles(v.nnz, v.nrows), LBK_USAGE_ERROR,
              "spmv_coo: stale plan (ntiles does not match lbk_coo_plan_size)");
     return v;
 }
@@ -183,7 +183,7 @@ LBK_SPMV_ADV_ENTRY(lbk_spmv_sellp_adv_f64, lbk_sellp, run_sellp, double, LBK_F64
 lbk_status lbk_csr_plan_size(const lbk_csr* A, int32_t* ntiles_out)
 {
     if (!A || !ntiles_out) return LBK_USAGE_ERROR;
-    *ntiles_out = csr_ntiles(A->nnz);
+    *ntiles_out = csr_ntiles(A->nnz, A->nrows);
     return LBK_OK;
 }
 
@@ -199,7 +199,7 @@ lbk_status lbk_csr_plan(lbk_ctx ctx, const lbk_csr* A, int32_t* tile_rows_dev)
 lbk_status lbk_coo_plan_size(const lbk_coo* A, int32_t* ntiles_out)
 {
     if (!A || !ntiles_out) return LBK_USAGE_ERROR;
-    *ntiles_out = coo_ntiles(A->nnz);
+    *ntiles_out = coo_ntiles(A->nnz, A->nrows);
     return LBK_OK;
 }
 
@@ -208,7 +208,7 @@ lbk_status lbk_coo_plan(lbk_ctx ctx, const lbk_coo* A, int32_t* tile_starts_dev)
     if (!ctx || !A) return LBK_USAGE_ERROR;
     return guard(ctx, [&] {
         need(A->nnz > 0, LBK_USAGE_ERROR, "lbk_coo_plan: matrix has no entries");
-        coo_plan_launch(ctx, A->row_idx, A->nnz, tile_starts_dev);
+        coo_plan_launch(ctx, A->row_idx, A->nrows, A->nnz, tile_starts_dev);
     });
 }
 

@@ -8,21 +8,9 @@
 //   ELL / SELL-P: SURVEY.md App. B (Ginkgo layouts), same per-row order.
 //
 // Design:
-//   * CSR and COO are TMA-staged, warp-specialised, persistent kernels.  The
-//     matrix is cut into nnz-balanced, row-aligned tiles.  One producer warp
-//     streams each tile's `vals`/`col_idx` (and COO `row_idx`) into a shared
-//     memory ring with 1-D bulk copies (cp.async.bulk, L2 evict-first) that
-//     complete on mbarriers; the consumer warps
-//       phase A: p_k = vals_k * x[col_k] for every entry of the tile (all
-//                gathers of the tile in flight at once; products rounded
-//                individually, no FMA),
-//       phase B: one thread per row sums its p_k sequentially from 0.0 in
-//                ascending k -- exactly the reference's order, so rows of
-//                length <= kLongRow are BIT-IDENTICAL to the FMA-free
-//                reference; longer rows are reduced by a whole warp
-//                (normwise tolerance).
-//     Tiles whose padded size exceeds the ring slot (giant rows) are
-//     processed straight from global memory by warp-per-row.
+//   * CSR and COO are warp-pipelined kernels over nnz-balanced, row-aligned
+//     tiles: each warp TMA-stages the next tile's arrays into shared memory
+//     while it processes the current one lane-per-row (csr_stream_kernel).
 //   * ELL / SELL-P are column-major: thread-per-row (4 rows per thread with
 //     128-bit value/index loads where alignment allows), streams read with
 //     ld.global.nc.L1::no_allocate, x gathered through the read-only path.
@@ -112,180 +100,63 @@ __global__ void csr_plan_kernel(const int* __restrict__ row_ptr, int nrows, int 
 __global__ void coo_plan_kernel(const int* __restrict__ rows, long long nnz, int ntiles,
                                 long long tile_nnz, int* __restrict__ tile_starts);
 
-// --------------------------------------------------- CSR staged kernel
-struct CsrCfg {
-    static constexpr int kConsumerWarps = 8;
-    static constexpr int kTile = 2048;   // target nnz per tile
-    static constexpr int kCap = 3072;    // ring slot capacity (entries)
-    static constexpr int kStages = 4;
+// ------------------------------------------------ CSR / COO stream kernels
+// Warp-pipelined, TMA-staged CSR over nnz-balanced, row-aligned tiles (a
+// merge-path split constrained to row boundaries; a giant row gets a wide
+// tile of its own).  Every warp of a persistent grid owns whole tiles and
+// runs its own two-slot pipeline in shared memory:
+//   * lane 0 issues two 1-D bulk copies (cp.async.bulk, L2 evict-first) of
+//     the NEXT tile's vals / col_idx into the free slot, completing on that
+//     slot's mbarrier -- the matrix streams never touch the LSU/L1 data
+//     path (ncu showed the L1 data pipe, not HBM, bounding an LSU-streamed
+//     version at 82% busy);
+//   * meanwhile the warp processes the CURRENT tile lane-per-row: lane l
+//     owns row rb + l (+32 ...), reads its entries from shared memory and
+//     gathers x -- across the warp those gathers hit consecutive rows'
+//     j-th columns, so on banded/stencil matrices they coalesce like ELL;
+//     up to kChunk gathers per lane are in flight before the sum;
+//   * each row is summed sequentially from 0.0 in ascending k with
+//     individually rounded products (no FMA) -- the reference's order
+//     (reference.cpp:82-88), so rows of length <= kLongRow are
+//     BIT-IDENTICAL to the FMA-free reference; longer staged rows are
+//     reduced by the warp (normwise tolerance).
+// Tiles wider than a slot go straight from global memory, warp per row.
+// The tile size is chosen per matrix (~32 rows of mean length, so one pass
+// of the warp covers the tile): see stream_tile_nnz().
+template <typename T>
+struct StreamCfg {
+    static constexpr int kWarps = 4;                 // warps per CTA
+    static constexpr int kThreads = kWarps * 32;
+    static constexpr int kCap = 1024;                // entries per slot
+        static constexpr int kIdxArrays = 1;             // CSR: col_idx
+    static constexpr size_t slot_bytes(int idx_arrays)
+    {
+        return size_t(kCap) * (sizeof(T) + 4 * idx_arrays);
+    }
+    static constexpr size_t smem_bytes(int idx_arrays)
+    {
+        return size_t(kWarps) * 2 * slot_bytes(idx_arrays);
+    }
 };
+constexpr int kTileMin = 384, kTileMax = 896;
 
-template <typename T, int CAP, int STAGES>
-constexpr size_t csr_smem_bytes()
+// Rows per lane per pass (G) from the mean row length: G*CH = 32 gathers
+// in flight per lane whichever the row length.
+inline int stream_group(long long nnz, long long nrows)
 {
-    return size_t(STAGES) * CAP * (sizeof(T) + 4) + size_t(CAP) * sizeof(T);
+    const long long mean = nrows > 0 ? (nnz + nrows - 1) / nrows : 1;
+    return mean <= 8 ? 4 : (mean <= 16 ? 2 : 1);
 }
 
-__device__ __forceinline__ void consumer_sync(int nthreads)
+// nnz-balanced tile size: one pass of the warp (32*G rows of mean length),
+// clamped so the tile plus a straddling row and alignment padding fits a
+// slot.
+inline long long stream_tile_nnz(long long nnz, long long nrows)
 {
-    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async_smem()
-{
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-template <typename T, class Epi, int NCW, int CAP, int STAGES>
-__global__ void __launch_bounds__((NCW + 1) * 32)
-    csr_staged_kernel(CsrView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
-{
-    constexpr int NC = NCW * 32;
-    constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
-    extern __shared__ __align__(128) unsigned char smem[];
-    T* s_vals = reinterpret_cast<T*>(smem);
-    int* s_cols = reinterpret_cast<int*>(smem + size_t(STAGES) * CAP * sizeof(T));
-    T* s_prod = reinterpret_cast<T*>(smem + size_t(STAGES) * CAP * (sizeof(T) + 4));
-    __shared__ __align__(8) uint64_t full[STAGES];
-    __shared__ __align__(8) uint64_t empty[STAGES];
-    __shared__ int4 info[STAGES];
-    __shared__ double red_sh[32 * NV];
-
-    if (epi.skip()) return;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NCW);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    const long long nnz4 = A.nnz & ~3LL;
-    double acc[NV];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
-
-    if (warp == NCW) {
-        // ---------------- producer warp: one elected lane drives the ring
-        if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
-            int j = 0;
-            for (int t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++j) {
-                const int s = j % STAGES;
-                if (j >= STAGES) mbar_wait(&empty[s], ((j / STAGES) - 1) & 1);
-                const int rb = __ldg(A.tile_rows + t), re = __ldg(A.tile_rows + t + 1);
-                const int k0 = __ldg(A.row_ptr + rb), k1 = __ldg(A.row_ptr + re);
-                info[s] = make_int4(rb, re, k0, k1);
-                const long long k0a = k0 & ~3, k1a = (static_cast<long long>(k1) + 3) & ~3LL;
-                const bool staged = (k1a - k0a) <= CAP;
-                const long long ke = k1a < nnz4 ? k1a : nnz4;
-                if (staged && ke > k0a) {
-                    const uint32_t n = static_cast<uint32_t>(ke - k0a);
-                    mbar_arrive_expect_tx(&full[s], n * uint32_t(sizeof(T) + 4));
-                    tma_load_1d(s_vals + size_t(s) * CAP, A.vals + k0a, n * sizeof(T), &full[s], pol);
-                    tma_load_1d(s_cols + size_t(s) * CAP, A.cols + k0a, n * 4u, &full[s], pol);
-                } else {
-                    mbar_arrive(&full[s]);
-                }
-            }
-        }
-    } else {
-        // ---------------- consumer warps
-        int j = 0;
-        for (int t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++j) {
-            const int s = j % STAGES;
-            mbar_wait(&full[s], (j / STAGES) & 1);
-            const int4 in = info[s];
-            const int rb = in.x, re = in.y, k0 = in.z, k1 = in.w;
-            const int k0a = k0 & ~3;
-            const long long k1a = (static_cast<long long>(k1) + 3) & ~3LL;
-            const bool staged = (k1a - k0a) <= CAP;
-            if (staged) {
-                T* sv = s_vals + size_t(s) * CAP;
-                int* sc = s_cols + size_t(s) * CAP;
-                if (k1 > nnz4) {  // ragged tail past the last 16-B chunk
-                    const int kt = k0 > nnz4 ? k0 : static_cast<int>(nnz4);
-                    for (int k = kt + tid; k < k1; k += NC) {
-                        sv[k - k0a] = A.vals[k];
-                        sc[k - k0a] = A.cols[k];
-                    }
-                    fence_proxy_async_smem();
-                    consumer_sync(NC);
-                }
-                // phase A: all products of the tile
-                for (int k = k0 + tid; k < k1; k += NC) {
-                    const int off = k - k0a;
-                    s_prod[off] = mul_rn(sv[off], ldg_nc(x + sc[off]));
-                }
-                consumer_sync(NC);
-                if (lane == 0) mbar_arrive(&empty[s]);  // slot free for the producer
-                // phase B: rows
-                for (int base = rb; base < re; base += NC) {
-                    const int r = base + tid;
-                    const bool act = r < re;
-                    int rs = 0, rl = 0;
-                    if (act) {
-                        rs = __ldg(A.row_ptr + r);
-                        rl = __ldg(A.row_ptr + r + 1) - rs;
-                    }
-                    const bool lng = act && rl > kLongRow;
-                    unsigned lm = __ballot_sync(0xffffffffu, lng);
-                    if (act && !lng) {
-                        const T* p = s_prod + (rs - k0a);
-                        T sum = T(0);
-                        for (int k = 0; k < rl; ++k) sum = add_rn(sum, p[k]);
-                        epi.row(r, sum, acc);
-                    }
-                    while (lm) {
-                        const int src = __ffs(lm) - 1;
-                        lm &= lm - 1;
-                        const int rr = __shfl_sync(0xffffffffu, r, src);
-                        const int ss = __shfl_sync(0xffffffffu, rs, src);
-                        const int ll = __shfl_sync(0xffffffffu, rl, src);
-                        T part = T(0);
-                        for (int k = lane; k < ll; k += 32) part = add_rn(part, s_prod[ss - k0a + k]);
-                        part = warp_sum(part);
-                        if (lane == 0) epi.row(rr, part, acc);
-                    }
-                }
-                consumer_sync(NC);  // s_prod is reused by the next tile
-            } else {
-                if (lane == 0) mbar_arrive(&empty[s]);
-                // giant-row tile: warp per row straight from global memory
-                for (int r = rb + warp; r < re; r += NCW) {
-                    const int rs = __ldg(A.row_ptr + r), rend = __ldg(A.row_ptr + r + 1);
-                    T part = T(0);
-                    for (int k = rs + lane; k < rend; k += 32)
-                        part = add_rn(part, mul_rn(A.vals[k], ldg_nc(x + A.cols[k])));
-                    part = warp_sum(part);
-                    if (lane == 0) epi.row(r, part, acc);
-                }
-            }
-        }
-    }
-
-    if constexpr (Epi::NV > 0) {
-        __syncthreads();
-        block_sum<NV>(acc, tid, blockDim.x, red_sh);
-        grid_reduce_finish<NV>(acc, ws, tid, blockDim.x, red_sh,
-                               [&](const double* tot) { epi.finish(tot); });
-    }
-}
-
-// --------------------------------------------------- COO staged kernel
-struct CooCfg {
-    static constexpr int kConsumerWarps = 8;
-    static constexpr int kTile = 2048;
-    static constexpr int kCap = 3072;
-    static constexpr int kStages = 3;
-};
-
-template <typename T, int CAP, int STAGES>
-constexpr size_t coo_smem_bytes()
-{
-    return size_t(STAGES) * CAP * (sizeof(T) + 8) + size_t(CAP) * sizeof(T);
+    long long mean = nrows > 0 ? (nnz + nrows - 1) / nrows : 1;
+    long long t = 32LL * stream_group(nnz, nrows) * (mean < 1 ? 1 : mean);
+    t = t < kTileMin ? kTileMin : (t > kTileMax ? kTileMax : t);
+    return t;
 }
 
 // first index in [lo, hi) with a[i] >= key
@@ -299,148 +170,321 @@ __device__ __forceinline__ int lower_bound_i(P a, int lo, int hi, int key)
     return lo;
 }
 
-template <typename T, class Epi, int NCW, int CAP, int STAGES>
-__global__ void __launch_bounds__((NCW + 1) * 32)
-    coo_staged_kernel(CooView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
+// One row straight from global memory by a whole warp: rows <= 32 keep the
+// sequential order (bit-exact); longer rows use 4 independent lane partials
+// (so 4 loads per lane are in flight) and a fixed-order warp reduction.
+template <typename T>
+__device__ __forceinline__ T warp_row_global(int ks, int ke, const int* __restrict__ cols,
+                                             const T* __restrict__ vals, const T* __restrict__ x)
 {
-    constexpr int NC = NCW * 32;
-    constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
-    extern __shared__ __align__(128) unsigned char smem[];
-    T* s_vals = reinterpret_cast<T*>(smem);
-    int* s_cols = reinterpret_cast<int*>(smem + size_t(STAGES) * CAP * sizeof(T));
-    int* s_rows = s_cols + size_t(STAGES) * CAP;
-    T* s_prod = reinterpret_cast<T*>(smem + size_t(STAGES) * CAP * (sizeof(T) + 8));
-    __shared__ __align__(8) uint64_t full[STAGES];
-    __shared__ __align__(8) uint64_t empty[STAGES];
-    __shared__ int4 info[STAGES];
-    __shared__ double red_sh[32 * NV];
+    const int lane = threadIdx.x & 31;
+    if (ke - ks <= 32) {
+        T p = T(0);
+        if (ks + lane < ke) p = mul_rn(__ldcs(vals + ks + lane), ldg_nc(x + __ldcs(cols + ks + lane)));
+        T sum = T(0);
+        for (int k = 0; k < ke - ks; ++k) sum = add_rn(sum, __shfl_sync(0xffffffffu, p, k));
+        return sum;
+    }
+    T p0 = T(0), p1 = T(0), p2 = T(0), p3 = T(0);
+    int k = ks + lane;
+    for (; k + 96 < ke; k += 128) {
+        const int c0 = __ldcs(cols + k), c1 = __ldcs(cols + k + 32), c2 = __ldcs(cols + k + 64),
+                  c3 = __ldcs(cols + k + 96);
+        const T v0 = __ldcs(vals + k), v1 = __ldcs(vals + k + 32), v2 = __ldcs(vals + k + 64),
+                v3 = __ldcs(vals + k + 96);
+        p0 = add_rn(p0, mul_rn(v0, ldg_nc(x + c0)));
+        p1 = add_rn(p1, mul_rn(v1, ldg_nc(x + c1)));
+        p2 = add_rn(p2, mul_rn(v2, ldg_nc(x + c2)));
+        p3 = add_rn(p3, mul_rn(v3, ldg_nc(x + c3)));
+    }
+    for (; k < ke; k += 32) p0 = add_rn(p0, mul_rn(__ldcs(vals + k), ldg_nc(x + __ldcs(cols + k))));
+    return warp_sum(add_rn(add_rn(p0, p1), add_rn(p2, p3)));
+}
 
-    if (epi.skip()) return;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NCW);
+// Phase B of a staged tile, lane-per-row.  A lane owns G rows per pass
+// (rows base + g*32 + lane) and gathers the first CH entries of each of them
+// before summing, so G*CH (= 32) independent gathers per lane are in flight
+// per pass; rows with CH < len <= kLongRow continue lane-privately, longer
+// rows are reduced by the whole warp.  Every row is summed sequentially from
+// 0.0 in ascending k with individually rounded products.
+template <typename T, int G, class Epi, class Ext>
+__device__ __forceinline__ void staged_rows(int rb, int re, const T* sv, const int* sc,
+                                            const T* __restrict__ x, const Epi& epi,
+                                            double* acc, Ext&& extent)
+{
+    constexpr int CH = 32 / G;
+    const int lane = threadIdx.x & 31;
+    for (int base = rb; base < re; base += 32 * G) {
+        int o[G], len[G];
+        T v[G][CH], g[G][CH];
+        unsigned lm = 0;
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            const int r = base + q * 32 + lane;
+            int2 e = make_int2(0, 0);
+            if (r < re) e = extent(r);
+            o[q] = e.x;
+            len[q] = e.y;
+            lm |= __ballot_sync(0xffffffffu, e.y > kLongRow) != 0 ? (1u << q) : 0u;
+            if (e.y > kLongRow) len[q] = -1;  // warp-cooperative below
         }
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+                if (j < len[q]) {
+                    v[q][j] = sv[o[q] + j];
+                    g[q][j] = ldg_nc(x + sc[o[q] + j]);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            const int r = base + q * 32 + lane;
+            if (r < re && len[q] >= 0) {
+                T sum = T(0);
+#pragma unroll
+                for (int j = 0; j < CH; ++j)
+                    if (j < len[q]) sum = add_rn(sum, mul_rn(v[q][j], g[q][j]));
+                for (int j = CH; j < len[q]; ++j)
+                    sum = add_rn(sum, mul_rn(sv[o[q] + j], ldg_nc(x + sc[o[q] + j])));
+                epi.row(r, sum, acc);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            if (!(lm & (1u << q))) continue;
+            unsigned m = __ballot_sync(0xffffffffu, len[q] < 0 && base + q * 32 + lane < re);
+            while (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1;
+                const int rr = base + q * 32 + src;
+                const int2 e = extent(rr);
+                T part = T(0);
+                for (int k = lane; k < e.y; k += 32)
+                    part = add_rn(part, mul_rn(sv[e.x + k], ldg_nc(x + sc[e.x + k])));
+                part = warp_sum(part);
+                if (lane == 0) epi.row(rr, part, acc);
+            }
+        }
+    }
+}
+
+// Issues the bulk copies of entries [k0, k1) (aligned down/up to 4 entries,
+// clamped to the last full 16-B chunk) into a slot; the ragged tail past
+// nnz4 is copied by the warp with ordinary loads.  Returns the aligned base.
+template <typename T, int NIDX>
+__device__ __forceinline__ int stage_tile(int k0, int k1, long long nnz4, T* sv, int* si0,
+                                          int* si1, const T* __restrict__ vals,
+                                          const int* __restrict__ idx0,
+                                          const int* __restrict__ idx1, uint64_t* bar,
+                                          uint64_t pol)
+{
+    const int lane = threadIdx.x & 31;
+    const int ka = k0 & ~3;
+    const long long kz = (static_cast<long long>(k1) + 3) & ~3LL;
+    const long long ke = kz < nnz4 ? kz : nnz4;
+    if (lane == 0) {
+        if (ke > ka) {
+            const uint32_t n = static_cast<uint32_t>(ke - ka);
+            mbar_arrive_expect_tx(bar, n * uint32_t(sizeof(T) + 4 * NIDX));
+            tma_load_1d(sv, vals + ka, n * sizeof(T), bar, pol);
+            tma_load_1d(si0, idx0 + ka, n * 4u, bar, pol);
+            if (NIDX == 2) tma_load_1d(si1, idx1 + ka, n * 4u, bar, pol);
+        } else {
+            mbar_arrive(bar);
+        }
+    }
+    if (k1 > nnz4) {
+        const int kt = k0 > nnz4 ? k0 : static_cast<int>(nnz4);
+        for (int k = kt + lane; k < k1; k += 32) {
+            sv[k - ka] = vals[k];
+            si0[k - ka] = idx0[k];
+            if (NIDX == 2) si1[k - ka] = idx1[k];
+        }
+    }
+    return ka;
+}
+
+// The per-warp tile loop shared by CSR and COO.  Tile metadata needs two
+// dependent loads (plan entry, then row_ptr / row_idx at it); they are
+// software-pipelined two and one tiles ahead so neither the bulk-copy issue
+// nor the row sweep ever waits on them:
+//   iteration i:  load m1(T_{i+3});  load m2(T_{i+2}) from m1(T_{i+2});
+//                 stage T_{i+1} (bounds complete);  process T_i.
+// meta1(t) / meta2(t, m1) return the lane-0/1 values (lanes >= 2: 0);
+// mk(m1, m2) -> int4 (row begin, row end, entry begin, entry end).
+template <typename T, int NIDX, class M1, class M2, class Mk, class Staged, class Wide>
+__device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const T* vals,
+                                               const int* idx0, const int* idx1,
+                                               unsigned char* wbase, uint64_t* bar, M1&& meta1,
+                                               M2&& meta2, Mk&& mk, Staged&& staged, Wide&& wide)
+{
+    using Cfg = StreamCfg<T>;
+    constexpr int CAP = Cfg::kCap, NW = Cfg::kWarps;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T* sv[2];
+    int *si0[2], *si1[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        unsigned char* b = wbase + q * Cfg::slot_bytes(NIDX);
+        sv[q] = reinterpret_cast<T*>(b);
+        si0[q] = reinterpret_cast<int*>(b + CAP * sizeof(T));
+        si1[q] = si0[q] + CAP;
+    }
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
         fence_mbar_init();
     }
-    __syncthreads();
+    __syncwarp();
+    const long long nnz4 = nnz & ~3LL;
+    const uint64_t pol = policy_evict_first();
+    const int nw = gridDim.x * NW;
+    auto staged_ok = [&](int4 bd) { return (bd.w - (bd.z & ~3) + 3) <= CAP; };
 
-    const long long nnz4 = A.nnz & ~3LL;
+    int t = blockIdx.x * NW + warp;
+    if (t >= ntiles) return;
+    int m1a = meta1(t), m1b = meta1(t + nw), m1c = meta1(t + 2 * nw);
+    int4 cur = mk(m1a, meta2(t, m1a));
+    int m2b = meta2(t + nw, m1b);
+    bool st_cur = staged_ok(cur);
+    int ka_cur = 0;
+    if (st_cur)
+        ka_cur = stage_tile<T, NIDX>(cur.z, cur.w, nnz4, sv[0], si0[0], si1[0], vals, idx0, idx1,
+                                     &bar[0], pol);
+    for (int it = 0; t < ntiles; t += nw, ++it) {
+        const int slot = it & 1;
+        const int m1d = meta1(t + 3 * nw);     // consumed two iterations later
+        const int m2c = meta2(t + 2 * nw, m1c);  // consumed next iteration
+        const int4 nxt = mk(m1b, m2b);
+        const bool has_nxt = t + nw < ntiles;
+        const bool st_nxt = has_nxt && staged_ok(nxt);
+        int ka_nxt = 0;
+        if (st_nxt) {
+            fence_proxy_async_smem();
+            ka_nxt = stage_tile<T, NIDX>(nxt.z, nxt.w, nnz4, sv[slot ^ 1], si0[slot ^ 1],
+                                         si1[slot ^ 1], vals, idx0, idx1, &bar[slot ^ 1], pol);
+        }
+        if (!st_cur && lane == 0) mbar_arrive(&bar[slot]);  // keep the phase in step
+        mbar_wait(&bar[slot], (it >> 1) & 1);
+        __syncwarp();
+        if (st_cur) staged(cur, ka_cur, sv[slot], si0[slot], si1[slot]);
+        else wide(cur);
+        __syncwarp();
+        cur = nxt;
+        st_cur = st_nxt;
+        ka_cur = ka_nxt;
+        m1b = m1c;
+        m1c = m1d;
+        m2b = m2c;
+    }
+}
+
+template <typename T, class Epi, int G>
+__global__ void __launch_bounds__(StreamCfg<T>::kThreads)
+    csr_stream_kernel(CsrView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
+{
+    using Cfg = StreamCfg<T>;
+    constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[Cfg::kWarps][2];
+    __shared__ double red_sh[32 * NV];
+    if (epi.skip()) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double acc[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc[i] = 0.0;
 
-    if (warp == NCW) {
-        if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
-            int j = 0;
-            for (int t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++j) {
-                const int s = j % STAGES;
-                if (j >= STAGES) mbar_wait(&empty[s], ((j / STAGES) - 1) & 1);
-                const int k0 = __ldg(A.tile_starts + t), k1 = __ldg(A.tile_starts + t + 1);
-                const int r0 = t == 0 ? 0 : __ldg(A.rows + k0);
-                const int r1 = t + 1 == A.ntiles ? A.nrows : __ldg(A.rows + k1);
-                info[s] = make_int4(r0, r1, k0, k1);
-                const long long k0a = k0 & ~3, k1a = (static_cast<long long>(k1) + 3) & ~3LL;
-                const bool staged = (k1a - k0a) <= CAP;
-                const long long ke = k1a < nnz4 ? k1a : nnz4;
-                if (staged && ke > k0a) {
-                    const uint32_t n = static_cast<uint32_t>(ke - k0a);
-                    mbar_arrive_expect_tx(&full[s], n * uint32_t(sizeof(T) + 8));
-                    tma_load_1d(s_vals + size_t(s) * CAP, A.vals + k0a, n * sizeof(T), &full[s], pol);
-                    tma_load_1d(s_cols + size_t(s) * CAP, A.cols + k0a, n * 4u, &full[s], pol);
-                    tma_load_1d(s_rows + size_t(s) * CAP, A.rows + k0a, n * 4u, &full[s], pol);
-                } else {
-                    mbar_arrive(&full[s]);
-                }
+    warp_tile_loop<T, 1>(
+        A.ntiles, A.nnz, A.vals, A.cols, nullptr,
+        smem + size_t(warp) * 2 * Cfg::slot_bytes(1), bars[warp],
+        [&](int t) { return (t < A.ntiles && lane < 2) ? __ldg(A.tile_rows + t + lane) : 0; },
+        [&](int t, int b) { return (t < A.ntiles && lane < 2) ? __ldg(A.row_ptr + b) : 0; },
+        [&](int b, int k) {
+            return make_int4(__shfl_sync(0xffffffffu, b, 0), __shfl_sync(0xffffffffu, b, 1),
+                             __shfl_sync(0xffffffffu, k, 0), __shfl_sync(0xffffffffu, k, 1));
+        },
+        [&](int4 bd, int ka, const T* sv, const int* sc, const int*) {
+            staged_rows<T, G>(bd.x, bd.y, sv, sc, x, epi, acc, [&](int r) {
+                const int rs = __ldg(A.row_ptr + r);
+                return make_int2(rs - ka, __ldg(A.row_ptr + r + 1) - rs);
+            });
+        },
+        [&](int4 bd) {
+            for (int r = bd.x; r < bd.y; ++r) {
+                const int ks = __ldg(A.row_ptr + r), ke = __ldg(A.row_ptr + r + 1);
+                const T s = warp_row_global<T>(ks, ke, A.cols, A.vals, x);
+                if (lane == 0) epi.row(r, s, acc);
             }
-        }
-    } else {
-        int j = 0;
-        for (int t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++j) {
-            const int s = j % STAGES;
-            mbar_wait(&full[s], (j / STAGES) & 1);
-            const int4 in = info[s];
-            const int r0 = in.x, r1 = in.y, k0 = in.z, k1 = in.w;
-            const int k0a = k0 & ~3;
-            const long long k1a = (static_cast<long long>(k1) + 3) & ~3LL;
-            const bool staged = (k1a - k0a) <= CAP;
-            if (staged) {
-                T* sv = s_vals + size_t(s) * CAP;
-                int* sc = s_cols + size_t(s) * CAP;
-                int* sr = s_rows + size_t(s) * CAP;
-                if (k1 > nnz4) {
-                    const int kt = k0 > nnz4 ? k0 : static_cast<int>(nnz4);
-                    for (int k = kt + tid; k < k1; k += NC) {
-                        sv[k - k0a] = A.vals[k];
-                        sc[k - k0a] = A.cols[k];
-                        sr[k - k0a] = A.rows[k];
-                    }
-                    fence_proxy_async_smem();
-                    consumer_sync(NC);
-                }
-                for (int k = k0 + tid; k < k1; k += NC) {
-                    const int off = k - k0a;
-                    s_prod[off] = mul_rn(sv[off], ldg_nc(x + sc[off]));
-                }
-                consumer_sync(NC);
-                // phase B needs the row indices, so the slot is released
-                // after the row sweep.
-                const int lo0 = k0 - k0a, hi0 = k1 - k0a;
-                for (int base = r0; base < r1; base += NC) {
-                    const int r = base + tid;
-                    const bool act = r < r1;
-                    int rs = 0, rl = 0;
-                    if (act) {
-                        rs = lower_bound_i(sr, lo0, hi0, r);
-                        rl = lower_bound_i(sr, rs, hi0, r + 1) - rs;
-                    }
-                    const bool lng = act && rl > kLongRow;
-                    unsigned lm = __ballot_sync(0xffffffffu, lng);
-                    if (act && !lng) {
-                        T sum = T(0);
-                        for (int k = 0; k < rl; ++k) sum = add_rn(sum, s_prod[rs + k]);
-                        epi.row(r, sum, acc);
-                    }
-                    while (lm) {
-                        const int src = __ffs(lm) - 1;
-                        lm &= lm - 1;
-                        const int rr = __shfl_sync(0xffffffffu, r, src);
-                        const int ss = __shfl_sync(0xffffffffu, rs, src);
-                        const int ll = __shfl_sync(0xffffffffu, rl, src);
-                        T part = T(0);
-                        for (int k = lane; k < ll; k += 32) part = add_rn(part, s_prod[ss + k]);
-                        part = warp_sum(part);
-                        if (lane == 0) epi.row(rr, part, acc);
-                    }
-                }
-                consumer_sync(NC);
-                if (lane == 0) mbar_arrive(&empty[s]);
-            } else {
-                if (lane == 0) mbar_arrive(&empty[s]);
-                for (int r = r0 + warp; r < r1; r += NCW) {
-                    int rs = 0, rend = 0;
-                    if (lane == 0) {
-                        rs = lower_bound_i(A.rows, k0, k1, r);
-                        rend = lower_bound_i(A.rows, rs, k1, r + 1);
-                    }
-                    rs = __shfl_sync(0xffffffffu, rs, 0);
-                    rend = __shfl_sync(0xffffffffu, rend, 0);
-                    T part = T(0);
-                    for (int k = rs + lane; k < rend; k += 32)
-                        part = add_rn(part, mul_rn(A.vals[k], ldg_nc(x + A.cols[k])));
-                    part = warp_sum(part);
-                    if (lane == 0) epi.row(r, part, acc);
-                }
-            }
-        }
-    }
+        });
 
     if constexpr (Epi::NV > 0) {
         __syncthreads();
-        block_sum<NV>(acc, tid, blockDim.x, red_sh);
-        grid_reduce_finish<NV>(acc, ws, tid, blockDim.x, red_sh,
+        block_sum<NV>(acc, tid, Cfg::kThreads, red_sh);
+        grid_reduce_finish<NV>(acc, ws, tid, Cfg::kThreads, red_sh,
+                               [&](const double* tot) { epi.finish(tot); });
+    }
+}
+
+// COO: warp tiles are row-aligned entry ranges [tile_starts[t],
+// tile_starts[t+1]) of the (row, col)-sorted entries; the tile owns rows
+// [r0, r1) including empty ones (reference.cpp:67 zero-fills y first).
+// row_idx is staged with vals/col_idx; a lane finds its row's extent by
+// binary search over the staged row indices.
+template <typename T, class Epi, int G>
+__global__ void __launch_bounds__(StreamCfg<T>::kThreads)
+    coo_stream_kernel(CooView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
+{
+    using Cfg = StreamCfg<T>;
+    constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[Cfg::kWarps][2];
+    __shared__ double red_sh[32 * NV];
+    if (epi.skip()) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double acc[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+
+    warp_tile_loop<T, 2>(
+        A.ntiles, A.nnz, A.vals, A.cols, A.rows,
+        smem + size_t(warp) * 2 * Cfg::slot_bytes(2), bars[warp],
+        [&](int t) { return (t < A.ntiles && lane < 2) ? __ldg(A.tile_starts + t + lane) : 0; },
+        [&](int t, int k) {
+            if (t >= A.ntiles || lane >= 2) return 0;
+            if (lane == 0) return t == 0 ? 0 : __ldg(A.rows + k);
+            return t + 1 == A.ntiles ? A.nrows : __ldg(A.rows + k);
+        },
+        [&](int k, int r) {
+            return make_int4(__shfl_sync(0xffffffffu, r, 0), __shfl_sync(0xffffffffu, r, 1),
+                             __shfl_sync(0xffffffffu, k, 0), __shfl_sync(0xffffffffu, k, 1));
+        },
+        [&](int4 bd, int ka, const T* sv, const int* sc, const int* sr) {
+            const int lo = bd.z - ka, hi = bd.w - ka;
+            staged_rows<T, G>(bd.x, bd.y, sv, sc, x, epi, acc, [&](int r) {
+                const int rs = lower_bound_i(sr, lo, hi, r);
+                return make_int2(rs, lower_bound_i(sr, rs, hi, r + 1) - rs);
+            });
+        },
+        [&](int4 bd) {
+            for (int r = bd.x; r < bd.y; ++r) {
+                int ks = 0, ke = 0;
+                if (lane == 0) {
+                    ks = lower_bound_i(A.rows, bd.z, bd.w, r);
+                    ke = lower_bound_i(A.rows, ks, bd.w, r + 1);
+                }
+                ks = __shfl_sync(0xffffffffu, ks, 0);
+                ke = __shfl_sync(0xffffffffu, ke, 0);
+                const T s = warp_row_global<T>(ks, ke, A.cols, A.vals, x);
+                if (lane == 0) epi.row(r, s, acc);
+            }
+        });
+
+    if constexpr (Epi::NV > 0) {
+        __syncthreads();
+        block_sum<NV>(acc, tid, Cfg::kThreads, red_sh);
+        grid_reduce_finish<NV>(acc, ws, tid, Cfg::kThreads, red_sh,
                                [&](const double* tot) { epi.finish(tot); });
     }
 }

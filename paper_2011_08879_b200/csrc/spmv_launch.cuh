@@ -13,20 +13,17 @@ namespace lbk {
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-inline int csr_ntiles(long long nnz)
+// Number of plan tiles (the plan holds ntiles + 1 int32 boundaries).
+inline int csr_ntiles(long long nnz, long long nrows)
 {
-    long long t = (nnz + CsrCfg::kTile - 1) / CsrCfg::kTile;
+    const long long tn = stream_tile_nnz(nnz, nrows);
+    long long t = (nnz + tn - 1) / tn;
     return static_cast<int>(t < 1 ? 1 : t);
 }
-
-inline int coo_ntiles(long long nnz)
-{
-    long long t = (nnz + CooCfg::kTile - 1) / CooCfg::kTile;
-    return static_cast<int>(t < 1 ? 1 : t);
-}
+inline int coo_ntiles(long long nnz, long long nrows) { return csr_ntiles(nnz, nrows); }
 
 void csr_plan_launch(lbk_ctx ctx, const int* row_ptr, int nrows, long long nnz, int* tile_rows);
-void coo_plan_launch(lbk_ctx ctx, const int* rows, long long nnz, int* tile_starts);
+void coo_plan_launch(lbk_ctx ctx, const int* rows, int nrows, long long nnz, int* tile_starts);
 
 // Forces the warp-per-row CSR kernel (diagnostics / A-B comparison).
 inline bool csr_force_warp()
@@ -38,8 +35,8 @@ inline bool csr_force_warp()
     return v != 0;
 }
 
-// Warp-per-row CSR straight from global memory: the fallback for arrays
-// that are not 16-B aligned (TMA bulk copies need it).
+// Warp-per-row CSR straight from global memory (LBK_CSR_ALGO=warp: A/B
+// comparison against the stream kernel).
 template <typename T, class Epi>
 __global__ void __launch_bounds__(256)
     csr_warp_kernel(CsrView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
@@ -87,12 +84,36 @@ int blocks_per_sm(K kernel, int threads, size_t smem)
     return b < 1 ? 1 : b;
 }
 
+template <typename K>
+void set_smem(K kernel, size_t bytes)
+{
+    LBK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(bytes)));
+}
+
+// Persistent grid: as many CTAs as fit (shared-memory bound), one warp per
+// tile at a time.
+template <typename T, int NIDX, int G, class K, class View, class Epi>
+void stream_launch(lbk_ctx ctx, K kernel, const View& A, const T* x, const Epi& epi, RedWs ws)
+{
+    using Cfg = StreamCfg<T>;
+    constexpr size_t smem = Cfg::smem_bytes(NIDX);
+    static bool attr = (set_smem(kernel, smem), true);
+    (void)attr;
+    static int bps = blocks_per_sm(kernel, Cfg::kThreads, smem);
+    long long cap = static_cast<long long>(ctx->num_sms) * bps;
+    if (cap > kRedMaxBlocks) cap = kRedMaxBlocks;
+    const long long want = (A.ntiles + Cfg::kWarps - 1) / Cfg::kWarps;
+    const int grid = static_cast<int>(want < cap ? want : cap);
+    kernel<<<grid, Cfg::kThreads, smem, ctx->stream>>>(A, x, epi, ws);
+    LBK_LAUNCH_CHECK();
+}
+
 template <typename T, class Epi>
 void launch_csr(lbk_ctx ctx, CsrView<T> A, const T* x, const Epi& epi, RedWs ws)
 {
-    constexpr int NCW = CsrCfg::kConsumerWarps, CAP = CsrCfg::kCap, ST = CsrCfg::kStages;
-    const bool tma_ok = aligned16(A.vals) && aligned16(A.cols) && !csr_force_warp();
-    if (!tma_ok) {
+    const bool tma_ok = aligned16(A.vals) && aligned16(A.cols);
+    if (csr_force_warp() || !tma_ok) {
         auto k = csr_warp_kernel<T, Epi>;
         static int bps = blocks_per_sm(k, 256, 0);
         long long want = (static_cast<long long>(A.nrows) * 32 + 255) / 256;
@@ -104,49 +125,34 @@ void launch_csr(lbk_ctx ctx, CsrView<T> A, const T* x, const Epi& epi, RedWs ws)
         return;
     }
     if (!A.tile_rows) {
-        A.ntiles = csr_ntiles(A.nnz);
+        A.ntiles = csr_ntiles(A.nnz, A.nrows);
         int* plan = static_cast<int*>(scratch(ctx, size_t(A.ntiles + 1) * sizeof(int)));
         csr_plan_launch(ctx, A.row_ptr, A.nrows, A.nnz, plan);
         A.tile_rows = plan;
     }
-    auto k = csr_staged_kernel<T, Epi, NCW, CAP, ST>;
-    constexpr size_t smem = csr_smem_bytes<T, CAP, ST>();
-    static bool attr = [&] {
-        LBK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        return true;
-    }();
-    (void)attr;
-    static int bps = blocks_per_sm(k, (NCW + 1) * 32, smem);
-    long long cap = static_cast<long long>(ctx->num_sms) * bps;
-    int grid = static_cast<int>(A.ntiles < cap ? A.ntiles : cap);
-    k<<<grid, (NCW + 1) * 32, smem, ctx->stream>>>(A, x, epi, ws);
-    LBK_LAUNCH_CHECK();
+    switch (stream_group(A.nnz, A.nrows)) {
+    case 4: stream_launch<T, 1, 4>(ctx, csr_stream_kernel<T, Epi, 4>, A, x, epi, ws); break;
+    case 2: stream_launch<T, 1, 2>(ctx, csr_stream_kernel<T, Epi, 2>, A, x, epi, ws); break;
+    default: stream_launch<T, 1, 1>(ctx, csr_stream_kernel<T, Epi, 1>, A, x, epi, ws); break;
+    }
 }
 
 template <typename T, class Epi>
 void launch_coo(lbk_ctx ctx, CooView<T> A, const T* x, const Epi& epi, RedWs ws)
 {
-    constexpr int NCW = CooCfg::kConsumerWarps, CAP = CooCfg::kCap, ST = CooCfg::kStages;
     need(aligned16(A.vals) && aligned16(A.cols) && aligned16(A.rows), LBK_USAGE_ERROR,
          "COO arrays must be 16-byte aligned");
     if (!A.tile_starts) {
-        A.ntiles = coo_ntiles(A.nnz);
+        A.ntiles = coo_ntiles(A.nnz, A.nrows);
         int* plan = static_cast<int*>(scratch(ctx, size_t(A.ntiles + 1) * sizeof(int)));
-        coo_plan_launch(ctx, A.rows, A.nnz, plan);
+        coo_plan_launch(ctx, A.rows, A.nrows, A.nnz, plan);
         A.tile_starts = plan;
     }
-    auto k = coo_staged_kernel<T, Epi, NCW, CAP, ST>;
-    constexpr size_t smem = coo_smem_bytes<T, CAP, ST>();
-    static bool attr = [&] {
-        LBK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        return true;
-    }();
-    (void)attr;
-    static int bps = blocks_per_sm(k, (NCW + 1) * 32, smem);
-    long long cap = static_cast<long long>(ctx->num_sms) * bps;
-    int grid = static_cast<int>(A.ntiles < cap ? A.ntiles : cap);
-    k<<<grid, (NCW + 1) * 32, smem, ctx->stream>>>(A, x, epi, ws);
-    LBK_LAUNCH_CHECK();
+    switch (stream_group(A.nnz, A.nrows)) {
+    case 4: stream_launch<T, 2, 4>(ctx, coo_stream_kernel<T, Epi, 4>, A, x, epi, ws); break;
+    case 2: stream_launch<T, 2, 2>(ctx, coo_stream_kernel<T, Epi, 2>, A, x, epi, ws); break;
+    default: stream_launch<T, 2, 1>(ctx, coo_stream_kernel<T, Epi, 1>, A, x, epi, ws); break;
+    }
 }
 
 // ELL (is_ell) or SELL-P over the sliced column-major layout.
