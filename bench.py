@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark of the B200 sparse backend.
+
+Metric (BASELINE.json): "FP64 CSR SpMV GB/s (% of HBM roofline) and CG
+iters/s at 1/2/4/8 B200".  A *step* is one CSR SpMV y = A x (reference
+spmv_csr, src/kernels/reference.cpp:74-89) over the config's matrix:
+
+  workload  cfg2 -- FP64 CSR SpMV, 3D 27-pt Poisson 128^3 (n = 2,097,152,
+            nnz = 55,742,968), x = seeded_values(n, 11) (harness.cpp:90-99);
+            the matrix is generated on the device (bit-exact vs the oracle,
+            tests/test_gpu_spmv.py).
+  value     algorithmic GB/s = (12 nnz + 4 (n+1) + 8 (n + n)) bytes per step
+            (reference byte model, harness.cpp:342-354) x N / device time,
+            inputs resident in HBM; matrix streams (670 MB) exceed L2, so no
+            flush is needed between steps (x, 16.8 MB, stays L2-resident as
+            it would inside a solver).
+  e2e       same metric through the C ABI (lbk_memcpy_h2d of x from pinned
+            host memory -> lbk_spmv_csr_f64 -> lbk_memcpy_d2h of y), copies
+            inside the timed region; the operator (matrix + plan) is set up
+            once, as the reference's clone_to does.
+  cg        CG iterations/s on cfg4 (7-pt Poisson 256^3, b = A*1, x0 = 0, tol
+            1e-8) with reference semantics (true residual every iteration)
+            and with the recurrence stop (verified true residual).
+N > 1 (torchrun): every rank runs the same SpMV replica on its own GPU (cfg1-3
+are single-GPU configs: "replicas only"); time = max over
+ranks; value = N x bytes / time ("scaling": "weak").
+
+--impl reference times the reference's own CPU implementation (oracle/_ref:
+the reference library compiled from /root/reference/proj/src, FMA-free) with
+ParallelExecutor(all host threads) on the same config; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 CSR SpMV GB/s (% of HBM roofline) and CG iters/s at 1/2/4/8 B200"
+WORKLOAD = {"workload": "cfg2: FP64 CSR SpMV, 3D 27-pt Poisson 128^3 (2,097,152 rows, "
+                        "55,742,968 nnz), single RHS",
+            "format": "csr", "matrix": "27pt-128^3", "rows": 2097152, "nnz": 55742968,
+            "l2": "inputs larger than L2 (matrix streams 670 MB > 126 MB); no flush"}
+PEAK_FALLBACK = 6650.0
+
+
+def csr_bytes(n: int, ncols: int, nnz: int) -> int:
+    """Reference byte model for CSR (harness.cpp:342-354)."""
+    return 12 * nnz + 4 * (n + 1) + 8 * (n + ncols)
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return PEAK_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch from the committed `ncu --set full` summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d["kernels"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed phases."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = f"/tmp/lbk_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, smax, reasons, util = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for row in csv.reader(f):
+                if len(row) < 8:
+                    continue
+                try:
+                    s, m, u = float(row[0]), float(row[1]), float(row[7])
+                except ValueError:
+                    continue
+                util.append(u)
+                if u < 50:  # only samples under load
+                    continue
+                sm.append(s)
+                smax.append(m)
+                for nm, v in zip(names, row[3:7]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples_under_load": len(sm)}
+
+
+# ------------------------------------------------------------ our arm
+def run_ours(args, rank: int, world: int, local_rank: int) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import ctypes as C
+
+    from paper_2011_08879_b200 import _lib as L, gen, larch as lk
+
+    torch.cuda.set_device(local_rank)
+    ex = lk.CudaExecutor(local_rank)
+    lib = L.load()
+    dev = ex.device
+
+    A = gen.stencil(ex, "27pt", 128)
+    n, nnz, ncols = A.nrows, A.nnz(), A.ncols
+    bytes_step = csr_bytes(n, A.ncols, nnz)
+    xh = gen.seeded_values(A.ncols, 11)
+    x = lk.vector_from(ex, xh)
+    y = lk.make_vector(ex, n)
+    desc = A.desc()  # builds + caches the load-balance plan once
+    xp, yp = C.c_void_p(x.values.data_ptr()), C.c_void_p(y.values.data_ptr())
+    ctx = ex.ctx
+    stream = ex.stream
+
+    def step():
+        st = lib.lbk_spmv_csr_f64(ctx, C.byref(desc), xp, yp)
+        if st:
+            lk._check(st, ctx)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region: K steps, one kernel each
+    K = args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(K)]
+    barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(K):
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    elapsed = t0.elapsed_time(t1) * 1e-3
+    launch_s = [a.elapsed_time(b) * 1e-3 for a, b in evs]
+    t_max = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    elapsed_max = float(t_max.item())
+
+    # ---- end-to-end through the C ABI with host buffers
+    xh_pin = torch.from_numpy(xh).pin_memory()
+    yh_pin = torch.empty(n, dtype=torch.float64).pin_memory()
+    xhp, yhp = C.c_void_p(xh_pin.data_ptr()), C.c_void_p(yh_pin.data_ptr())
+    nb = 8 * n
+
+    def e2e_step():
+        lk._check(lib.lbk_memcpy_h2d(ctx, xp, xhp, 8 * ncols), ctx)
+        step()
+        lk._check(lib.lbk_memcpy_d2h(ctx, yhp, yp, nb), ctx)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_t.item())
+
+    # ---- CG iterations/s (cfg4), replica per rank
+    cg = None
+    if not args.no_cg:
+        del A, desc
+        torch.cuda.empty_cache()
+        A4 = gen.stencil(ex, "7pt", 256)
+        ones = lk.vector_from(ex, np.ones(A4.ncols))
+        b = lk.make_vector(ex, A4.nrows)
+        lk.spmv(A4, ones, b)  # b = A*1 (harness.cpp:376-378); rows <= 32 -> bit-exact
+        cg = {"config": "cfg4: 7-pt Poisson 256^3, b = A*1, x0 = 0, tol 1e-8"}
+        for mode in ("true", "recurrence"):
+            xs = lk.zeros(ex, A4.nrows)
+            r = lk.solve(A4, b, xs, lk.SolverConfig(kind="cg", rel_tol=1e-8, max_iters=20000,
+                                                      residual_mode=mode))
+            tt = torch.tensor([r.elapsed], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            el = float(tt.item())
+            cg[mode] = {"iterations": r.iterations, "golden_iterations": 581,
+                        "final_rel_residual": r.final_rel_residual, "seconds": el,
+                        "iters_per_s": world * r.iterations / el,
+                        "gflops_ref_model": world * r.flop_count / el / 1e9}
+        del A4, ones, b, xs
+    clocks = sampler.stop()
+
+    if rank != 0:
+        return
+    value = world * bytes_step * K / elapsed_max
+    peak, peak_src = measured_peak()
+    avg_launch = sum(launch_s) / len(launch_s)
+    achieved = bytes_step / avg_launch / 1e9
+    traffic = ncu_traffic("csr_stream_kernel")
+    line = {
+        "metric": METRIC, "value": round(value / 1e9, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": elapsed_max / K * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (App. B 27-pt stencil generated on device; x = seeded_values(n, 11))",
+        "config": dict(WORKLOAD, parallelism=f"replicas x{world}"),
+        "gflops": round(world * 2 * nnz * K / elapsed_max / 1e9, 1),
+        "roofline": {"bound": "hbm", "kernel": "csr_stream_kernel", "achieved": round(achieved, 1),
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "frac_of_8000": round(achieved / 8000, 4),
+                     "traffic": traffic, "algorithmic_bytes_per_launch": bytes_step,
+                     "avg_launch_us": avg_launch * 1e6},
+        "e2e": {"value": round(world * bytes_step * K / e2e_s / 1e9, 2), "unit": "GB/s",
+                "h2d_bytes_per_step": 8 * ncols, "d2h_bytes_per_step": nb,
+                "ms_per_step": e2e_s / K * 1e3,
+                "path": "lbk_memcpy_h2d(x) + lbk_spmv_csr_f64 + lbk_memcpy_d2h(y), pinned host"},
+        "gpu_launches": K,
+        "clocks": clocks,
+    }
+    if cg is not None:
+        line["cg"] = cg
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_sample()
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ CPU legs
+def _cfg2_host():
+    from oracle import oracle as O
+    return O, O.stencil("27pt", 128)
+
+
+def cpu_baseline_sample(reps: int = 5) -> dict:
+    """The reference library (oracle/_ref) on this host's cores: median of
+    `reps` cfg2 CSR SpMVs with ParallelExecutor(nproc)."""
+    try:
+        O, A = _cfg2_host()
+        if not O.ref_available():
+            raise RuntimeError("oracle/_ref not built")
+        cores = os.cpu_count() or 1
+        x = O.seeded_values(A.ncols, 11)
+        _, med = O.ref_spmv(A, x, "csr", exec_kind=O.EXEC_PARALLEL, workers=cores, reps=reps)
+        return {"value": round(csr_bytes(A.nrows, A.ncols, A.nnz) / med / 1e9, 3), "unit": "GB/s",
+                "cores": cores, "kind": "reference",
+                "sample": f"cfg2 CSR SpMV, reference ParallelExecutor({cores}), median of {reps}",
+                "ms_per_step": med * 1e3}
+    except Exception as e:  # reported, never fatal for the GPU arm
+        return {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                "sample": f"unavailable: {e}"}
+
+
+def run_reference(args, rank: int) -> None:
+    if rank != 0:
+        return
+    O, A = _cfg2_host()
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    cores = os.cpu_count() or 1
+    x = O.seeded_values(A.ncols, 11)
+    for _ in range(args.warmup):
+        O.ref_spmv(A, x, "csr", exec_kind=O.EXEC_PARALLEL, workers=cores, reps=1)
+    times = []
+    for _ in range(args.steps):
+        _, s = O.ref_spmv(A, x, "csr", exec_kind=O.EXEC_PARALLEL, workers=cores, reps=1)
+        times.append(s)
+    total = sum(times)
+    b = csr_bytes(A.nrows, A.ncols, A.nnz)
+    v = round(b * len(times) / total / 1e9, 3)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total / len(times) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (App. B 27-pt stencil, oracle generator)",
+            "config": dict(WORKLOAD, parallelism=f"host ParallelExecutor({cores})"),
+            "gflops": round(2 * A.nnz * len(times) / total / 1e9, 3),
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "reference",
+                             "sample": f"cfg2 CSR SpMV through the reference's spmv_csr, "
+                                       f"{len(times)} steps"},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cg", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

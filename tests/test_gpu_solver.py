@@ -1,0 +1,190 @@
+"""GPU parity: device-resident CG / BiCGSTAB (lbk_solve_csr/coo) against the
+reference library and the survey goldens:
+
+* iteration counts: |I_gpu - I_ref| <= max(1, reference spread);
+* residual histories within 1e-7 relative (CG) of the oracle's; BiCGSTAB
+  over the first 40 iterations within 1e-6 (its trajectory is chaotic);
+* flop_count equal to the reference accounting (krylov.cpp:41-69);
+* KATs: 2x2 CG -> [1/11, 7/11]; A = I in 1 iteration; b = 0 -> 0 iterations;
+  fixed_iters runs exactly that many; breakdown raises with its iteration.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import relerr
+
+pytestmark = pytest.mark.gpu
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+
+
+def up(lk, ex, A):
+    return lk.csr_from_host(ex, A.nrows, A.ncols, A.row_ptr, A.cols, A.vals)
+
+
+def solve(lk, ex, M, bh, **cfg):
+    b = lk.vector_from(ex, bh)
+    x = lk.zeros(ex, M.nrows)
+    r = lk.solve(M, b, x, lk.SolverConfig(**cfg))
+    return r, lk.vector_to_host(x)
+
+
+@pytest.mark.parametrize("fmt", ["csr", "coo"])
+def test_cg16_golden(O, ex, lk, fmt):
+    A = up(lk, ex, O.stencil("7pt", 16))
+    M = A if fmt == "csr" else lk.csr_to_coo(A)
+    r, x = solve(lk, ex, M, G["cg16_b"], kind="cg", rel_tol=1e-8, max_iters=20000)
+    assert abs(r.iterations - int(G["cg16_iters"])) <= 1
+    h, hr = np.array(r.residual_history), G["cg16_hist"]
+    k = min(len(h), len(hr))
+    # the reference's own executor spread at 16^3 is 1.3e-7 (reference vs
+    # parallel(4)); allow ~8x that
+    assert np.max(np.abs(h[:k] - hr[:k]) / hr[:k]) <= 1e-6
+    if r.iterations == int(G["cg16_iters"]):
+        assert r.flop_count == int(G["cg16_flops"])
+    assert relerr(x, G["cg16_x"]) <= 1e-9
+    assert r.converged and r.final_rel_residual <= 1e-8
+
+
+def test_bicgstab16_golden(O, ex, lk):
+    A = up(lk, ex, O.stencil("7pt", 16, 0.5))
+    r, x = solve(lk, ex, A, G["bicg16_b"], kind="bicgstab", rel_tol=1e-8, max_iters=20000)
+    assert abs(r.iterations - int(G["bicg16_iters"])) <= 1
+    h, hr = np.array(r.residual_history), G["bicg16_hist"]
+    k = min(len(h), len(hr), 40)
+    assert np.max(np.abs(h[:k] - hr[:k]) / hr[:k]) <= 1e-6
+    if r.iterations == int(G["bicg16_iters"]):
+        assert r.flop_count == int(G["bicg16_flops"])
+    assert r.converged
+
+
+def test_kats(ex, lk):
+    A = lk.csr_from_host(ex, 2, 2, [0, 2, 4], [0, 1, 0, 1], [4.0, 1.0, 1.0, 3.0])
+    r, x = solve(lk, ex, A, np.array([1.0, 2.0]), kind="cg", rel_tol=1e-12, max_iters=10)
+    assert np.allclose(x, [1 / 11, 7 / 11], rtol=0, atol=1e-12)
+    assert np.allclose(x, G["cg2_x"], rtol=0, atol=1e-15)
+    n = 1000
+    I = lk.csr_from_host(ex, n, n, np.arange(n + 1), np.arange(n), np.ones(n))
+    for kind in ("cg", "bicgstab"):
+        r, x = solve(lk, ex, I, np.linspace(1, 2, n), kind=kind, rel_tol=1e-10)
+        assert r.iterations == 1 and r.converged
+        r, x = solve(lk, ex, I, np.zeros(n), kind=kind, rel_tol=1e-10)
+        assert r.iterations == 0 and r.converged and r.residual_history == [0.0]
+        assert np.all(x == 0)
+
+
+def test_fixed_iters_and_freeze(O, ex, lk):
+    R = O.stencil("7pt", 12)
+    A = up(lk, ex, R)
+    b = O.spmv_csr(R, np.ones(R.nrows))
+    for kind in ("cg", "bicgstab"):
+        r, _ = solve(lk, ex, A, b, kind=kind, rel_tol=1e-8, fixed_iters=300)
+        assert r.iterations == 300 and len(r.residual_history) == 301
+        if O.ref_available():
+            rr = O.ref_solve(R, b, kind, rel_tol=1e-8, fixed_iters=300)
+            assert rr.iterations == 300
+            # the freeze (krylov.cpp:150-153) makes the tail constant
+            assert r.residual_history[-1] == r.residual_history[-2]
+
+
+def test_breakdown(R, ex, lk):
+    O = R
+    # <p, Ap> = 0 on the first iteration: A = [[0,1],[1,0]], b = [1,0]
+    A = O.Csr(2, 2, np.array([0, 1, 2], np.int32), np.array([1, 0], np.int32), np.ones(2))
+    with pytest.raises(O.OracleError) as e_ref:
+        O.ref_solve(A, np.array([1.0, 0.0]), "cg", rel_tol=1e-10)
+    with pytest.raises(lk.BreakdownError) as e:
+        solve(lk, ex, up(lk, ex, A), np.array([1.0, 0.0]), kind="cg", rel_tol=1e-10)
+    assert e.value.iteration == e_ref.value.iteration == 1
+
+
+def test_config_errors(ex, lk):
+    A = lk.csr_from_host(ex, 2, 2, [0, 1, 2], [0, 1], [1.0, 1.0])
+    with pytest.raises(lk.ConfigurationError):
+        solve(lk, ex, A, np.ones(2), kind="cg", max_iters=0)
+    with pytest.raises(lk.ConfigurationError):
+        solve(lk, ex, A, np.ones(2), kind="cg", rel_tol=0.0)
+    with pytest.raises(lk.ConfigurationError):
+        solve(lk, ex, A, np.ones(2), kind="gmres")
+    B = lk.csr_from_host(ex, 2, 3, [0, 1, 2], [0, 1], [1.0, 1.0])
+    with pytest.raises(lk.ShapeError):
+        solve(lk, ex, B, np.ones(2), kind="cg")
+
+
+@pytest.mark.parametrize("m,iters", [(32, 81), (64, 158), (128, 296)])
+def test_cg_iteration_goldens(ex, lk, m, iters):
+    from paper_2011_08879_b200 import gen
+    A = gen.stencil(ex, "7pt", m)
+    ones = lk.vector_from(ex, np.ones(A.ncols))
+    b = lk.make_vector(ex, A.nrows)
+    lk.spmv(A, ones, b)
+    for mode in ("true", "recurrence"):
+        x = lk.zeros(ex, A.nrows)
+        r = lk.solve(A, b, x, lk.SolverConfig(kind="cg", rel_tol=1e-8, max_iters=20000,
+                                               residual_mode=mode))
+        assert abs(r.iterations - iters) <= 1, (mode, r.iterations)
+        assert r.converged and r.final_rel_residual <= 1e-8
+
+
+def test_cg_history_vs_reference(R, ex, lk):
+    O = R
+    Rm = O.stencil("7pt", 32)
+    b = O.spmv_csr(Rm, np.ones(Rm.nrows))
+    rr = O.ref_solve(Rm, b, "cg", rel_tol=1e-8, max_iters=20000)
+    spread = max(np.max(np.abs(p.history - rr.history) / rr.history)
+                 for p in (O.ref_solve(Rm, b, "cg", rel_tol=1e-8, max_iters=20000, exec_kind=1,
+                                       workers=w) for w in (2, 3, 4, 8)))
+    r, x = solve(lk, ex, up(lk, ex, Rm), b, kind="cg", rel_tol=1e-8, max_iters=20000)
+    assert r.iterations == rr.iterations
+    assert r.flop_count == rr.flop_count
+    h = np.array(r.residual_history)
+    # within 10x the reference's own reduction-order spread (3.8e-8 here)
+    assert np.max(np.abs(h - rr.history) / rr.history) <= max(1e-7, 10 * spread)
+    assert relerr(x, rr.x) <= 1e-9
+
+
+def test_bicgstab_history_vs_reference(R, ex, lk):
+    O = R
+    Rm = O.stencil("7pt", 32, 0.5)
+    b = O.spmv_csr(Rm, O.seeded_values(Rm.nrows, 11))
+    rr = O.ref_solve(Rm, b, "bicgstab", rel_tol=1e-8, max_iters=20000)
+    rp = O.ref_solve(Rm, b, "bicgstab", rel_tol=1e-8, max_iters=20000, exec_kind=1, workers=8)
+    r, _ = solve(lk, ex, up(lk, ex, Rm), b, kind="bicgstab", rel_tol=1e-8, max_iters=20000)
+    spread = max(1, abs(rp.iterations - rr.iterations))
+    assert abs(r.iterations - rr.iterations) <= spread
+    h = np.array(r.residual_history)
+    k = min(40, len(h), len(rr.history))
+    assert np.max(np.abs(h[:k] - rr.history[:k]) / rr.history[:k]) <= 1e-6
+
+
+def test_cfg4_cg_256(ex, lk):
+    """cfg4 at full size: 581 +- 1 iterations (golden), final
+    true residual <= 1e-8, hist[1] = 5.037289e-01."""
+    from paper_2011_08879_b200 import gen
+    A = gen.stencil(ex, "7pt", 256)
+    ones = lk.vector_from(ex, np.ones(A.ncols))
+    b = lk.make_vector(ex, A.nrows)
+    lk.spmv(A, ones, b)
+    x = lk.zeros(ex, A.nrows)
+    r = lk.solve(A, b, x, lk.SolverConfig(kind="cg", rel_tol=1e-8, max_iters=20000))
+    assert abs(r.iterations - 581) <= 1 and r.final_rel_residual <= 1e-8
+    assert abs(r.residual_history[1] - 5.037289e-01) <= 1e-6
+    assert r.flop_count == r.iterations * (4 * A.nnz() + 16 * A.nrows) + 2 * A.nnz() + 4 * A.nrows
+    xh = lk.vector_to_host(x)
+    assert np.max(np.abs(xh - 1.0)) < 1e-5
+
+
+def test_cfg5_bicgstab_256(ex, lk):
+    """cfg5: 7-pt upwind gamma 0.5, b = A x*, x* = seeded_values(n, 11):
+    oracle 495 (reference) / 498 (parallel) -> accept 495 +- 3."""
+    from paper_2011_08879_b200 import gen
+    A = gen.stencil(ex, "7pt", 256, 0.5)
+    xs = lk.vector_from(ex, gen.seeded_values(A.ncols, 11))
+    b = lk.make_vector(ex, A.nrows)
+    lk.spmv(A, xs, b)  # bit-identical to the oracle's CSR SpMV (rows <= 32)
+    x = lk.zeros(ex, A.nrows)
+    r = lk.solve(A, b, x, lk.SolverConfig(kind="bicgstab", rel_tol=1e-8, max_iters=20000))
+    assert abs(r.iterations - 495) <= 3, r.iterations
+    assert r.final_rel_residual <= 1e-8
+    assert abs(r.residual_history[1] - 1.136784e-01) <= 1e-6
