@@ -249,6 +249,71 @@ lbk_status lbk_solve_coo(lbk_ctx, const lbk_coo* A, const double* b, double* x,
                          const lbk_solver_cfg* cfg, lbk_solve_result* result,
                          double* history, int32_t history_cap);
 
+/* ------------------------------------------------- distributed (new) */
+/* Row-partitioned CSR over P ranks (the reference has no
+ * distributed matrix).  Partition: contiguous row blocks,
+ * rank(r) = min(r / ceil(N/P), P-1).  Host-side maps (no device needed):
+ * build the map from the rank's own rows (global column ids), exchange
+ * ghost lists with the peers (an all-to-all the caller runs over its own
+ * bootstrap, e.g. torch.distributed), hand the requests back with
+ * lbk_dist_map_set_sends, then create the device matrix.  Vectors the
+ * operator is applied to must hold n_local + n_ghost doubles (the halo
+ * lands behind the owned part). */
+typedef struct lbk_dist_map_s* lbk_dist_map;
+typedef struct lbk_dist_csr_s* lbk_dist_csr;
+typedef struct lbk_comm_s* lbk_comm;
+typedef struct lbk_dist_map_info_t {
+    int32_t begin, end, n_local, n_ghost, n_interior, n_boundary;
+    int64_t nnz_local;
+    int32_t n_send; /* -1 until lbk_dist_map_set_sends */
+} lbk_dist_map_info_t;
+
+lbk_status lbk_part_range(int32_t n, int32_t nparts, int32_t rank, int32_t* begin, int32_t* end);
+/* row_ptr: local, n_local + 1 entries starting at 0; cols: GLOBAL ids. */
+lbk_status lbk_dist_map_create(int32_t n_global, int32_t ncols_global, int32_t nparts,
+                               int32_t rank, int32_t n_local, const int32_t* row_ptr,
+                               const int32_t* cols, lbk_dist_map* out);
+lbk_status lbk_dist_map_info(lbk_dist_map m, lbk_dist_map_info_t* info);
+/* ghosts: sorted global ids [n_ghost]; ghost_off [nparts+1]: the ghosts
+ * owned by rank q are ghosts[ghost_off[q] .. ghost_off[q+1]). */
+lbk_status lbk_dist_map_ghosts(lbk_dist_map m, int32_t* ghosts, int32_t* ghost_off);
+/* local column ids: owned c -> c - begin, ghost -> n_local + ghost index. */
+lbk_status lbk_dist_map_local_cols(lbk_dist_map m, int32_t* local_cols);
+lbk_status lbk_dist_map_rows(lbk_dist_map m, int32_t* interior, int32_t* boundary);
+/* req_off[nparts+1], req_gids: the global ids peer q requested from this
+ * rank (q's ghost_off run for this rank), strictly increasing per peer. */
+lbk_status lbk_dist_map_set_sends(lbk_dist_map m, const int32_t* req_off, const int32_t* req_gids);
+lbk_status lbk_dist_map_sends(lbk_dist_map m, int32_t* send_off, int32_t* send_idx);
+lbk_status lbk_dist_map_destroy(lbk_dist_map m);
+
+/* Communicators: NCCL (one process per GPU; the 128-byte unique id comes
+ * from rank 0 over the caller's bootstrap) or an in-process thread group
+ * (P host threads, each with its own lbk_ctx; used for P virtual ranks on
+ * one device and for single-process multi-GPU). */
+lbk_status lbk_comm_nccl_unique_id(void* id_out /* 128 bytes */);
+lbk_status lbk_comm_init_nccl(const void* id, int32_t nranks, int32_t rank, int32_t device,
+                              lbk_comm* out);
+lbk_status lbk_comm_init_threads(int32_t nranks, lbk_comm* comms_out /* [nranks] */);
+lbk_status lbk_comm_destroy(lbk_comm c);
+lbk_status lbk_comm_allreduce_sum_f64(lbk_ctx ctx, lbk_comm comm, double* dev, int32_t count);
+
+/* Device matrix from the map + this rank's row_ptr (local) and values
+ * (HOST arrays); n_global_nnz feeds the reference flop accounting. */
+lbk_status lbk_dist_csr_create(lbk_ctx ctx, lbk_dist_map m, const int32_t* row_ptr,
+                               const double* vals, int64_t n_global_nnz, lbk_dist_csr* out);
+lbk_status lbk_dist_csr_info(lbk_dist_csr D, int32_t* n_local, int32_t* n_ghost);
+lbk_status lbk_dist_csr_destroy(lbk_dist_csr D);
+/* y[n_local] <- A x; x_ext[n_local + n_ghost] (halo filled by the call):
+ * pack -> ncclSend/ncclRecv on a comm stream overlapped with the interior
+ * rows -> boundary rows.  Collective: every rank calls it. */
+lbk_status lbk_dist_spmv_f64(lbk_ctx ctx, lbk_dist_csr D, lbk_comm comm, double* x_ext, double* y);
+/* Distributed solve (CG / BiCGSTAB, lbk_solver_cfg as lbk_solve_csr): b, x
+ * are the rank's n_local parts; dot products are reduced over ranks, so
+ * every rank sees the same iterations, history and result.  Collective. */
+lbk_status lbk_dist_solve(lbk_ctx ctx, lbk_dist_csr D, lbk_comm comm, const double* b, double* x,
+                          const lbk_solver_cfg* cfg, lbk_solve_result* result, double* history,
+                          int32_t history_cap);
+
 /* ------------------------------------------------ synthetic inputs */
 /* Benchmark configurations; input synthesis, not
  * part of the measured path.  kind 0 = 2D 5-pt (m x m), 1 = 3D 7-pt

@@ -58,6 +58,12 @@ class lbk_sellp(C.Structure):
                 ("col_idx", C.c_void_p), ("vals", C.c_void_p)]
 
 
+class lbk_dist_map_info_t(C.Structure):
+    _fields_ = [("begin", C.c_int32), ("end", C.c_int32), ("n_local", C.c_int32),
+                ("n_ghost", C.c_int32), ("n_interior", C.c_int32), ("n_boundary", C.c_int32),
+                ("nnz_local", C.c_int64), ("n_send", C.c_int32)]
+
+
 class lbk_solver_cfg(C.Structure):
     _fields_ = [("kind", C.c_int32), ("max_iters", C.c_int32), ("rel_tol", C.c_double),
                 ("fixed_iters", C.c_int32), ("residual_mode", C.c_int32)]
@@ -127,6 +133,25 @@ SIGNATURES = {
     "lbk_validate_coo": (st, [vp, P(lbk_coo)]),
     "lbk_solve_csr": (st, [vp, P(lbk_csr), vp, vp, P(lbk_solver_cfg), P(lbk_solve_result), vp, i32]),
     "lbk_solve_coo": (st, [vp, P(lbk_coo), vp, vp, P(lbk_solver_cfg), P(lbk_solve_result), vp, i32]),
+    "lbk_part_range": (st, [i32, i32, i32, P(i32), P(i32)]),
+    "lbk_dist_map_create": (st, [i32, i32, i32, i32, i32, vp, vp, P(vp)]),
+    "lbk_dist_map_info": (st, [vp, P(lbk_dist_map_info_t)]),
+    "lbk_dist_map_ghosts": (st, [vp, vp, vp]),
+    "lbk_dist_map_local_cols": (st, [vp, vp]),
+    "lbk_dist_map_rows": (st, [vp, vp, vp]),
+    "lbk_dist_map_set_sends": (st, [vp, vp, vp]),
+    "lbk_dist_map_sends": (st, [vp, vp, vp]),
+    "lbk_dist_map_destroy": (st, [vp]),
+    "lbk_comm_nccl_unique_id": (st, [vp]),
+    "lbk_comm_init_nccl": (st, [vp, i32, i32, i32, P(vp)]),
+    "lbk_comm_init_threads": (st, [i32, vp]),
+    "lbk_comm_destroy": (st, [vp]),
+    "lbk_comm_allreduce_sum_f64": (st, [vp, vp, vp, i32]),
+    "lbk_dist_csr_create": (st, [vp, vp, vp, vp, i64, P(vp)]),
+    "lbk_dist_csr_info": (st, [vp, P(i32), P(i32)]),
+    "lbk_dist_csr_destroy": (st, [vp]),
+    "lbk_dist_spmv_f64": (st, [vp, vp, vp, vp, vp]),
+    "lbk_dist_solve": (st, [vp, vp, vp, vp, vp, P(lbk_solver_cfg), P(lbk_solve_result), vp, i32]),
     "lbk_gen_stencil_nnz": (i64, [C.c_int, C.c_int]),
     "lbk_gen_stencil_csr": (st, [vp, C.c_int, C.c_int, f64, vp, vp, vp]),
     "lbk_gen_seeded_values": (None, [i64, C.c_uint64, vp]),

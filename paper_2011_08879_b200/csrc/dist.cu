@@ -1,0 +1,471 @@
+// dist.cu -- row-partitioned distributed CSR: partition/halo maps (host,
+// bit-exact with the App. B restatement in oracle/port.cpp), the two
+// communicator back ends, device setup and the overlapped SpMV entry point.
+// See dist.cuh for the layout.
+#include <algorithm>
+#include <barrier>
+#include <cstring>
+#include <memory>
+#include <mutex>
+
+#include "api_guard.h"
+#include "dist.cuh"
+
+namespace lbk {
+namespace {
+
+void part_range(int n, int P, int rank, int* b, int* e)
+{
+    const long long chunk = (static_cast<long long>(n) + P - 1) / P;
+    long long lo = std::min<long long>(static_cast<long long>(rank) * chunk, n);
+    long long hi = rank == P - 1 ? n : std::min<long long>((rank + 1) * chunk, n);
+    *b = static_cast<int>(lo);
+    *e = static_cast<int>(hi);
+}
+
+#define LBK_NCCL(call)                                                                     \
+    do {                                                                                   \
+        ncclResult_t r_ = (call);                                                          \
+        if (r_ != ncclSuccess)                                                             \
+            ::lbk::fail(LBK_NCCL_ERROR, std::string(#call ": ") + ncclGetErrorString(r_)); \
+    } while (0)
+
+// ------------------------------------------------------------ NCCL
+// One process per GPU (torchrun); the unique id travels over the caller's
+// bootstrap (torch.distributed broadcast).  Halo exchange = grouped
+// ncclSend/ncclRecv on the comm stream; dots = ncclAllReduce(sum).
+struct NcclComm final : Comm {
+    ncclComm_t comm = nullptr;
+    ~NcclComm() override
+    {
+        if (comm) ncclCommDestroy(comm);
+    }
+    void allreduce_sum(double* dev, int count, cudaStream_t s) override
+    {
+        LBK_NCCL(ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, comm, s));
+    }
+    void exchange(const double* send_buf, const std::vector<int>& so, double* recv,
+                  const std::vector<int>& ro, cudaStream_t s) override
+    {
+        LBK_NCCL(ncclGroupStart());
+        for (int q = 0; q < nranks; ++q) {
+            if (q == rank) continue;
+            const int ns = so[q + 1] - so[q], nr = ro[q + 1] - ro[q];
+            if (ns > 0) LBK_NCCL(ncclSend(send_buf + so[q], ns, ncclDouble, q, comm, s));
+            if (nr > 0) LBK_NCCL(ncclRecv(recv + ro[q], nr, ncclDouble, q, comm, s));
+        }
+        LBK_NCCL(ncclGroupEnd());
+    }
+    bool async() const override { return true; }
+};
+
+// ------------------------------------------------------------ threads
+// In-process SPMD group: P host threads, each driving its own lbk_ctx (on
+// the same or on different devices), meet at host barriers.  Used for
+// P virtual ranks on one GPU (the partition / halo / reduction logic runs
+// exactly as with NCCL) and for single-process multi-GPU runs.  Allreduce
+// sums the per-rank values in rank order on the host, so every rank gets
+// the same bits; exchanges are device-to-device copies from the peers'
+// send buffers.
+struct ThreadShared {
+    int P;
+    std::barrier<> bar;
+    std::vector<double> slots[2];
+    std::vector<const double*> send_bufs;
+    std::vector<const std::vector<int>*> send_offs;
+    explicit ThreadShared(int p) : P(p), bar(p), send_bufs(p), send_offs(p)
+    {
+        slots[0].resize(size_t(p) * 32);
+        slots[1].resize(size_t(p) * 32);
+    }
+};
+
+struct ThreadComm final : Comm {
+    std::shared_ptr<ThreadShared> sh;
+    int parity = 0;
+    void allreduce_sum(double* dev, int count, cudaStream_t s) override
+    {
+        need(count <= 32, LBK_USAGE_ERROR, "thread allreduce: at most 32 values");
+        auto& slot = sh->slots[parity];
+        parity ^= 1;
+        LBK_CUDA(cudaMemcpyAsync(slot.data() + size_t(rank) * 32, dev, count * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
+        LBK_CUDA(cudaStreamSynchronize(s));
+        sh->bar.arrive_and_wait();
+        double tot[32];
+        for (int i = 0; i < count; ++i) tot[i] = 0.0;
+        for (int q = 0; q < nranks; ++q)
+            for (int i = 0; i < count; ++i) tot[i] += slot[size_t(q) * 32 + i];
+        LBK_CUDA(cudaMemcpyAsync(dev, tot, count * sizeof(double), cudaMemcpyHostToDevice, s));
+        LBK_CUDA(cudaStreamSynchronize(s));
+    }
+    void exchange(const double* send_buf, const std::vector<int>& so, double* recv,
+                  const std::vector<int>& ro, cudaStream_t s) override
+    {
+        LBK_CUDA(cudaStreamSynchronize(s));  // pack finished
+        sh->send_bufs[rank] = send_buf;
+        sh->send_offs[rank] = &so;
+        sh->bar.arrive_and_wait();
+        for (int q = 0; q < nranks; ++q) {
+            const int nr = ro[q + 1] - ro[q];
+            if (q == rank || nr == 0) continue;
+            const auto& pso = *sh->send_offs[q];
+            need(pso[rank + 1] - pso[rank] == nr, LBK_INTERNAL,
+                 "halo exchange: send/recv counts disagree");
+            LBK_CUDA(cudaMemcpyAsync(recv + ro[q], sh->send_bufs[q] + pso[rank],
+                                     size_t(nr) * sizeof(double), cudaMemcpyDefault, s));
+        }
+        LBK_CUDA(cudaStreamSynchronize(s));
+        sh->bar.arrive_and_wait();  // peers may reuse their send buffers
+    }
+    bool async() const override { return false; }
+};
+
+__global__ void pack_kernel(int n, const int* __restrict__ idx, const double* __restrict__ x,
+                            double* __restrict__ out)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = x[__ldg(idx + i)];
+}
+
+lbk_dist_map_s* map_of(lbk_dist_map m)
+{
+    need(m != nullptr, LBK_USAGE_ERROR, "null distributed map");
+    return m;
+}
+
+// Builds one row-subset sub-matrix (rows `rows`, columns already local).
+void build_sub(lbk_ctx ctx, SubCsr& S, const std::vector<int>& rows, const int32_t* row_ptr,
+               const std::vector<int>& lcols, const double* vals, int ncols)
+{
+    std::vector<int> rp(rows.size() + 1, 0), cols;
+    std::vector<double> v;
+    for (size_t i = 0; i < rows.size(); ++i) {
+        const int r = rows[i];
+        for (int k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
+            cols.push_back(lcols[k]);
+            v.push_back(vals[k]);
+        }
+        rp[i + 1] = static_cast<int>(cols.size());
+    }
+    S.nrows = static_cast<int>(rows.size());
+    S.ncols = ncols;
+    S.nnz = static_cast<long long>(cols.size());
+    S.row_ptr.alloc(rp.size() * 4);
+    S.cols.alloc(cols.size() * 4);
+    S.vals.alloc(v.size() * 8);
+    S.row_map.alloc(rows.size() * 4);
+    LBK_CUDA(cudaMemcpy(S.row_ptr.p, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice));
+    if (!cols.empty()) {
+        LBK_CUDA(cudaMemcpy(S.cols.p, cols.data(), cols.size() * 4, cudaMemcpyHostToDevice));
+        LBK_CUDA(cudaMemcpy(S.vals.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice));
+    }
+    if (!rows.empty())
+        LBK_CUDA(cudaMemcpy(S.row_map.p, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice));
+    if (S.nrows > 0) {
+        S.ntiles = csr_ntiles(S.nnz, S.nrows);
+        S.plan.alloc(size_t(S.ntiles + 1) * 4);
+        csr_plan_launch(ctx, S.row_ptr.as<int>(), S.nrows, S.nnz, S.plan.as<int>());
+    }
+}
+
+}  // namespace
+
+void dist_pack(lbk_ctx ctx, const lbk_dist_csr_s* D, const double* x)
+{
+    const int n = D->send_off.back();
+    if (n == 0) return;
+    pack_kernel<<<ceil_div(n, 256) < 1184 ? ceil_div(n, 256) : 1184, 256, 0, ctx->stream>>>(
+        n, D->send_idx.as<int>(), x, D->send_buf.as<double>());
+    LBK_LAUNCH_CHECK();
+}
+
+}  // namespace lbk
+
+using namespace lbk;
+
+extern "C" {
+
+lbk_status lbk_part_range(int32_t n, int32_t nparts, int32_t rank, int32_t* begin, int32_t* end)
+{
+    if (!begin || !end || n < 0 || nparts < 1 || rank < 0 || rank >= nparts)
+        return LBK_USAGE_ERROR;
+    part_range(n, nparts, rank, begin, end);
+    return LBK_OK;
+}
+
+lbk_status lbk_dist_map_create(int32_t n_global, int32_t ncols_global, int32_t nparts,
+                               int32_t rank, int32_t n_local, const int32_t* row_ptr,
+                               const int32_t* cols, lbk_dist_map* out)
+{
+    if (!out) return LBK_USAGE_ERROR;
+    return guard(nullptr, [&] {
+        need(nparts >= 1 && rank >= 0 && rank < nparts, LBK_USAGE_ERROR,
+             "dist map: rank outside [0, nparts)");
+        need(n_global == ncols_global, LBK_SHAPE_ERROR,
+             "dist map: the row partition is applied to x, so the matrix must be square");
+        auto m = std::make_unique<lbk_dist_map_s>();
+        m->n_global = n_global;
+        m->ncols_global = ncols_global;
+        m->P = nparts;
+        m->rank = rank;
+        part_range(n_global, nparts, rank, &m->begin, &m->end);
+        m->n_local = m->end - m->begin;
+        need(n_local == m->n_local, LBK_SHAPE_ERROR,
+             "dist map: n_local " + std::to_string(n_local) + " != partition size " +
+                 std::to_string(m->n_local));
+        need(row_ptr != nullptr && row_ptr[0] == 0, LBK_FORMAT_ERROR,
+             "dist map: local row_ptr must start at 0");
+        const long long nnz = row_ptr[n_local];
+        m->nnz_local = nnz;
+        const int b = m->begin, e = m->end;
+        for (long long k = 0; k < nnz; ++k) {
+            const int c = cols[k];
+            need(c >= 0 && c < ncols_global, LBK_FORMAT_ERROR, "dist map: column out of range");
+            if (c < b || c >= e) m->ghosts.push_back(c);
+        }
+        std::sort(m->ghosts.begin(), m->ghosts.end());
+        m->ghosts.erase(std::unique(m->ghosts.begin(), m->ghosts.end()), m->ghosts.end());
+        m->ghost_off.assign(nparts + 1, 0);
+        {
+            size_t g = 0;
+            for (int q = 0; q < nparts; ++q) {
+                int qb, qe;
+                part_range(n_global, nparts, q, &qb, &qe);
+                m->ghost_off[q] = static_cast<int>(g);
+                while (g < m->ghosts.size() && m->ghosts[g] < qe) ++g;
+            }
+            m->ghost_off[nparts] = static_cast<int>(m->ghosts.size());
+        }
+        m->local_cols.resize(static_cast<size_t>(nnz));
+        for (int r = 0; r < n_local; ++r) {
+            bool ghost = false;
+            for (int k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
+                const int c = cols[k];
+                if (c >= b && c < e) {
+                    m->local_cols[k] = c - b;
+                } else {
+                    ghost = true;
+                    m->local_cols[k] =
+                        n_local + static_cast<int>(std::lower_bound(m->ghosts.begin(), m->ghosts.end(), c) -
+                                                   m->ghosts.begin());
+                }
+            }
+            (ghost ? m->boundary : m->interior).push_back(r);
+        }
+        *out = m.release();
+    });
+}
+
+lbk_status lbk_dist_map_info(lbk_dist_map m, lbk_dist_map_info_t* info)
+{
+    if (!m || !info) return LBK_USAGE_ERROR;
+    info->begin = m->begin;
+    info->end = m->end;
+    info->n_local = m->n_local;
+    info->n_ghost = static_cast<int32_t>(m->ghosts.size());
+    info->n_interior = static_cast<int32_t>(m->interior.size());
+    info->n_boundary = static_cast<int32_t>(m->boundary.size());
+    info->nnz_local = m->nnz_local;
+    info->n_send = m->sends_set ? m->send_off.back() : -1;
+    return LBK_OK;
+}
+
+lbk_status lbk_dist_map_ghosts(lbk_dist_map m, int32_t* ghosts, int32_t* ghost_off)
+{
+    if (!m) return LBK_USAGE_ERROR;
+    if (ghosts && !m->ghosts.empty())
+        std::memcpy(ghosts, m->ghosts.data(), m->ghosts.size() * 4);
+    if (ghost_off) std::memcpy(ghost_off, m->ghost_off.data(), m->ghost_off.size() * 4);
+    return LBK_OK;
+}
+
+lbk_status lbk_dist_map_local_cols(lbk_dist_map m, int32_t* local_cols)
+{
+    if (!m || !local_cols) return LBK_USAGE_ERROR;
+    if (!m->local_cols.empty())
+        std::memcpy(local_cols, m->local_cols.data(), m->local_cols.size() * 4);
+    return LBK_OK;
+}
+
+lbk_status lbk_dist_map_rows(lbk_dist_map m, int32_t* interior, int32_t* boundary)
+{
+    if (!m) return LBK_USAGE_ERROR;
+    if (interior && !m->interior.empty())
+        std::memcpy(interior, m->interior.data(), m->interior.size() * 4);
+    if (boundary && !m->boundary.empty())
+        std::memcpy(boundary, m->boundary.data(), m->boundary.size() * 4);
+    return LBK_OK;
+}
+
+lbk_status lbk_dist_map_set_sends(lbk_dist_map m, const int32_t* req_off, const int32_t* req_gids)
+{
+    if (!m || !req_off) return LBK_USAGE_ERROR;
+    return guard(nullptr, [&] {
+        need(req_off[0] == 0, LBK_FORMAT_ERROR, "send requests: offsets must start at 0");
+        m->send_off.assign(req_off, req_off + m->P + 1);
+        m->send_idx.resize(static_cast<size_t>(req_off[m->P]));
+        for (int q = 0; q < m->P; ++q) {
+            need(req_off[q + 1] >= req_off[q], LBK_FORMAT_ERROR, "send requests: offsets decrease");
+            need(q != m->rank || req_off[q + 1] == req_off[q], LBK_FORMAT_ERROR,
+                 "send requests: a rank cannot request from itself");
+            for (int i = req_off[q]; i < req_off[q + 1]; ++i) {
+                const int g = req_gids[i];
+                need(g >= m->begin && g < m->end, LBK_FORMAT_ERROR,
+                     "send requests: global id " + std::to_string(g) + " not owned by rank " +
+                         std::to_string(m->rank));
+                need(i == req_off[q] || req_gids[i - 1] < g, LBK_FORMAT_ERROR,
+                     "send requests: ids must be strictly increasing per peer");
+                m->send_idx[i] = g - m->begin;
+            }
+        }
+        m->sends_set = true;
+    });
+}
+
+lbk_status lbk_dist_map_sends(lbk_dist_map m, int32_t* send_off, int32_t* send_idx)
+{
+    if (!m || !m->sends_set) return LBK_USAGE_ERROR;
+    if (send_off) std::memcpy(send_off, m->send_off.data(), m->send_off.size() * 4);
+    if (send_idx && !m->send_idx.empty())
+        std::memcpy(send_idx, m->send_idx.data(), m->send_idx.size() * 4);
+    return LBK_OK;
+}
+
+lbk_status lbk_dist_map_destroy(lbk_dist_map m)
+{
+    delete m;
+    return LBK_OK;
+}
+
+// ------------------------------------------------------------ comms
+lbk_status lbk_comm_nccl_unique_id(void* id_out)
+{
+    if (!id_out) return LBK_USAGE_ERROR;
+    return guard(nullptr, [&] {
+        ncclUniqueId id;
+        LBK_NCCL(ncclGetUniqueId(&id));
+        std::memcpy(id_out, &id, sizeof(id));
+    });
+}
+
+lbk_status lbk_comm_init_nccl(const void* id, int32_t nranks, int32_t rank, int32_t device,
+                              lbk_comm* out)
+{
+    if (!id || !out) return LBK_USAGE_ERROR;
+    return guard(nullptr, [&] {
+        LBK_CUDA(cudaSetDevice(device));
+        auto c = std::make_unique<NcclComm>();
+        c->nranks = nranks;
+        c->rank = rank;
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof(uid));
+        LBK_NCCL(ncclCommInitRank(&c->comm, nranks, uid, rank));
+        auto h = std::make_unique<lbk_comm_s>();
+        h->impl = c.release();
+        *out = h.release();
+    });
+}
+
+lbk_status lbk_comm_init_threads(int32_t nranks, lbk_comm* comms_out)
+{
+    if (!comms_out || nranks < 1) return LBK_USAGE_ERROR;
+    return guard(nullptr, [&] {
+        auto sh = std::make_shared<ThreadShared>(nranks);
+        for (int r = 0; r < nranks; ++r) {
+            auto c = std::make_unique<ThreadComm>();
+            c->nranks = nranks;
+            c->rank = r;
+            c->sh = sh;
+            auto h = std::make_unique<lbk_comm_s>();
+            h->impl = c.release();
+            comms_out[r] = h.release();
+        }
+    });
+}
+
+lbk_status lbk_comm_destroy(lbk_comm c)
+{
+    if (c) {
+        delete c->impl;
+        delete c;
+    }
+    return LBK_OK;
+}
+
+lbk_status lbk_comm_allreduce_sum_f64(lbk_ctx ctx, lbk_comm comm, double* dev, int32_t count)
+{
+    if (!ctx || !comm) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] { comm->impl->allreduce_sum(dev, count, ctx->stream); });
+}
+
+// ------------------------------------------------------------ matrix
+lbk_status lbk_dist_csr_create(lbk_ctx ctx, lbk_dist_map m, const int32_t* row_ptr,
+                               const double* vals, int64_t n_global_nnz, lbk_dist_csr* out)
+{
+    if (!ctx || !out) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        map_of(m);
+        need(m->sends_set, LBK_USAGE_ERROR,
+             "dist csr: call lbk_dist_map_set_sends (ghost-list all-to-all) first");
+        need(row_ptr != nullptr && row_ptr[m->n_local] == m->nnz_local, LBK_FORMAT_ERROR,
+             "dist csr: row_ptr does not match the map");
+        auto D = std::make_unique<lbk_dist_csr_s>();
+        D->n_local = m->n_local;
+        D->n_ghost = static_cast<int>(m->ghosts.size());
+        D->P = m->P;
+        D->rank = m->rank;
+        D->nnz_local = m->nnz_local;
+        D->n_global = m->n_global;
+        D->nnz_global = n_global_nnz;
+        D->device = ctx->device;
+        const int next = m->n_local + D->n_ghost;
+        build_sub(ctx, D->interior, m->interior, row_ptr, m->local_cols, vals, m->n_local);
+        build_sub(ctx, D->boundary, m->boundary, row_ptr, m->local_cols, vals, next);
+        D->send_off = m->send_off;
+        D->recv_off = m->ghost_off;
+        const size_t ns = m->send_idx.size();
+        D->send_idx.alloc(ns * 4);
+        D->send_buf.alloc(ns * 8);
+        if (ns)
+            LBK_CUDA(cudaMemcpy(D->send_idx.p, m->send_idx.data(), ns * 4, cudaMemcpyHostToDevice));
+        LBK_CUDA(cudaStreamCreateWithFlags(&D->comm_stream, cudaStreamNonBlocking));
+        LBK_CUDA(cudaEventCreateWithFlags(&D->ev_pack, cudaEventDisableTiming));
+        LBK_CUDA(cudaEventCreateWithFlags(&D->ev_recv, cudaEventDisableTiming));
+        LBK_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = D.release();
+    });
+}
+
+lbk_status lbk_dist_csr_info(lbk_dist_csr D, int32_t* n_local, int32_t* n_ghost)
+{
+    if (!D) return LBK_USAGE_ERROR;
+    if (n_local) *n_local = D->n_local;
+    if (n_ghost) *n_ghost = D->n_ghost;
+    return LBK_OK;
+}
+
+lbk_status lbk_dist_csr_destroy(lbk_dist_csr D)
+{
+    if (D) {
+        cudaSetDevice(D->device);
+        if (D->comm_stream) cudaStreamDestroy(D->comm_stream);
+        if (D->ev_pack) cudaEventDestroy(D->ev_pack);
+        if (D->ev_recv) cudaEventDestroy(D->ev_recv);
+        delete D;
+    }
+    return LBK_OK;
+}
+
+lbk_status lbk_dist_spmv_f64(lbk_ctx ctx, lbk_dist_csr D, lbk_comm comm, double* x_ext, double* y)
+{
+    if (!ctx || !D) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        need(D->P == 1 || (comm && comm->impl->nranks == D->P && comm->impl->rank == D->rank),
+             LBK_USAGE_ERROR, "dist spmv: communicator does not match the partition");
+        dist_apply(ctx, D, comm ? comm->impl : nullptr, x_ext, EpiStore<double>{y}, RedWs{},
+                   RedWs{});
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,146 @@
+// dist.cuh -- row-partitioned distributed CSR (absent from the
+// reference, whose only "communication" is in-process copy routing,
+// device_array.cpp:144-201).
+//
+//   partition  contiguous row blocks, rank(r) = min(r / ceil(N/P), P-1)
+//   ghosts     sorted unique non-owned columns of the rank's rows; ghost g
+//              gets local column id n_local + g; ghosts owned by rank q form
+//              one contiguous run (ghost_off[q], ghost_off[q+1])
+//   sends      for each peer q, the local ids q needs from us (q's ghosts we
+//              own, ascending) -- learned by one all-to-all of ghost lists
+//   rows       interior rows (no ghost column) and boundary rows, each kept
+//              as a CSR sub-matrix over the extended vector
+//              x_ext = [x_local | x_ghost] with a row map back to local rows
+//   SpMV       pack send values -> exchange (NCCL send/recv on a comm stream)
+//              overlapped with the interior rows -> boundary rows.  Each row
+//              keeps the reference's ascending-k order (boundary rows see
+//              their columns renumbered, but ghost ids preserve the global
+//              column order, so the k order is unchanged).
+#pragma once
+
+#include <nccl.h>
+
+#include <vector>
+
+#include "spmv_launch.cuh"
+
+struct lbk_dist_map_s {
+    int n_global, ncols_global, P, rank, begin, end, n_local;
+    long long nnz_local;
+    std::vector<int> ghosts;      // sorted global ids
+    std::vector<int> ghost_off;   // P + 1
+    std::vector<int> local_cols;  // nnz_local
+    std::vector<int> interior, boundary;
+    std::vector<int> send_off;    // P + 1
+    std::vector<int> send_idx;    // local ids
+    bool sends_set = false;
+};
+
+namespace lbk {
+
+// Cross-rank operations the distributed path needs.
+struct Comm {
+    int nranks = 1, rank = 0;
+    virtual ~Comm() = default;
+    // sum `count` doubles at dev over all ranks, result on every rank (same
+    // bits everywhere), stream-ordered on s
+    virtual void allreduce_sum(double* dev, int count, cudaStream_t s) = 0;
+    // halo exchange: send_buf[send_off[q] .. send_off[q+1]) goes to rank q;
+    // from rank q we receive recv_off[q+1]-recv_off[q] values into
+    // recv + recv_off[q].  Stream-ordered on s.
+    virtual void exchange(const double* send_buf, const std::vector<int>& send_off,
+                          double* recv, const std::vector<int>& recv_off, cudaStream_t s) = 0;
+    // true if exchange() is asynchronous on s (can overlap compute on
+    // another stream)
+    virtual bool async() const = 0;
+};
+
+struct DevArr {
+    void* p = nullptr;
+    ~DevArr()
+    {
+        if (p) cudaFree(p);
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+    void alloc(size_t bytes)
+    {
+        LBK_CUDA(cudaMalloc(&p, bytes < 16 ? 16 : bytes));
+    }
+};
+
+struct SubCsr {
+    int nrows = 0, ncols = 0;
+    long long nnz = 0;
+    DevArr row_ptr, cols, vals, row_map, plan;
+    int ntiles = 0;
+    CsrView<double> view() const
+    {
+        return CsrView<double>{nrows, ncols, nnz, row_ptr.as<int>(), cols.as<int>(),
+                               vals.as<double>(), plan.as<int>(), ntiles};
+    }
+};
+
+// Epilogue adaptor: sub-matrix row -> local row.
+template <class Epi>
+struct MappedEpi {
+    static constexpr int NV = Epi::NV;
+    Epi e;
+    const int* __restrict__ map;
+    __device__ bool skip() const { return e.skip(); }
+    __device__ void row(int r, double s, double* acc) const { e.row(__ldg(map + r), s, acc); }
+    __device__ void finish(const double* t) const { e.finish(t); }
+};
+
+}  // namespace lbk
+
+struct lbk_dist_csr_s {
+    int n_local = 0, n_ghost = 0, P = 1, rank = 0;
+    long long nnz_local = 0, n_global = 0, nnz_global = 0;
+    lbk::SubCsr interior, boundary;
+    std::vector<int> send_off, recv_off;
+    lbk::DevArr send_idx, send_buf;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_pack = nullptr, ev_recv = nullptr;
+    int device = 0;
+};
+
+struct lbk_comm_s {
+    lbk::Comm* impl = nullptr;
+};
+
+namespace lbk {
+
+void dist_pack(lbk_ctx ctx, const lbk_dist_csr_s* D, const double* x);
+
+// y = A x_ext with the halo exchange overlapped with the interior rows.
+// `epi` reduces over interior rows into ws_a.out and boundary rows into
+// ws_b.out when the RedWs are deferred (the solver path).
+template <class Epi>
+void dist_apply(lbk_ctx ctx, lbk_dist_csr_s* D, Comm* comm, double* x_ext, const Epi& epi,
+                RedWs ws_a, RedWs ws_b)
+{
+    const bool xchg = comm && comm->nranks > 1;
+    if (xchg) {
+        dist_pack(ctx, D, x_ext);
+        if (comm->async()) {
+            LBK_CUDA(cudaEventRecord(D->ev_pack, ctx->stream));
+            LBK_CUDA(cudaStreamWaitEvent(D->comm_stream, D->ev_pack, 0));
+            comm->exchange(D->send_buf.as<double>(), D->send_off, x_ext + D->n_local, D->recv_off,
+                           D->comm_stream);
+            LBK_CUDA(cudaEventRecord(D->ev_recv, D->comm_stream));
+        } else {
+            comm->exchange(D->send_buf.as<double>(), D->send_off, x_ext + D->n_local, D->recv_off,
+                           ctx->stream);
+        }
+    }
+    if (D->interior.nrows > 0)
+        launch_csr<double>(ctx, D->interior.view(), x_ext, MappedEpi<Epi>{epi, D->interior.row_map.as<int>()},
+                           ws_a);
+    if (xchg && comm->async()) LBK_CUDA(cudaStreamWaitEvent(ctx->stream, D->ev_recv, 0));
+    if (D->boundary.nrows > 0)
+        launch_csr<double>(ctx, D->boundary.view(), x_ext, MappedEpi<Epi>{epi, D->boundary.row_map.as<int>()},
+                           ws_b);
+}
+
+}  // namespace lbk

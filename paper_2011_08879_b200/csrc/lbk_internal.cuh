@@ -72,6 +72,9 @@ struct RedWs {
     double* partials;     // [max_blocks * slots]
     unsigned* counter;    // zero between uses
     double* out;          // [slots] device result
+    int defer = 0;        // 1: the finisher only stores the grid totals to
+                          // `out` (a cross-rank allreduce runs before the
+                          // epilogue's finish(), see dist.cu)
 };
 RedWs red_ws(lbk_ctx ctx, int max_blocks, int slots);
 
@@ -235,7 +238,12 @@ __device__ __forceinline__ bool grid_reduce_finish(const double (&v)[NV], RedWs 
     __syncthreads();
     block_sum<NV>(acc, tid, nthreads, sh);
     if (tid == 0) {
-        fin(acc);
+        if (ws.defer) {
+#pragma unroll
+            for (int i = 0; i < NV; ++i) ws.out[i] = acc[i];
+        } else {
+            fin(acc);
+        }
         *ws.counter = 0;
     }
     return true;

@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "api_guard.h"
+#include "dist.cuh"
 #include "spmv_launch.cuh"
 
 namespace lbk {
@@ -550,9 +551,112 @@ const char* breakdown_what(int w)
     }
 }
 
-template <class Op>
-void solve_impl(lbk_ctx ctx, const Op& op, long long n, long long nnz, const double* b, double* x,
-                const lbk_solver_cfg* cfg, lbk_solve_result* res, double* history, int hist_cap)
+// Single-device environment: the fused kernels reduce and finish in one
+// launch (RedWs.defer = 0).
+template <class MatOp>
+struct LocalEnv {
+    lbk_ctx ctx;
+    MatOp op;
+    RedWs ws;
+    long long n, nnz;
+    long long n_local() const { return n; }
+    long long n_ext() const { return n; }
+    long long n_global() const { return n; }
+    long long nnz_global() const { return nnz; }
+    bool ext_x() const { return false; }
+    template <class Epi>
+    void apply(const double* x, const Epi& e) { op.apply(ctx, x, e, ws); }
+    template <class Op>
+    void vec(const Op& o) { launch_vec(ctx, n, o, ws); }
+    double norm(const double* b)
+    {
+        double v = 0.0;
+        if (lbk_nrm2_f64(ctx, n, b, &v) != LBK_OK) fail(LBK_CUDA_ERROR, ctx->err);
+        return v;
+    }
+};
+
+// Distributed environment: every reduction is deferred --
+// the fused kernels leave their local totals in ws.out, a one-warp kernel
+// combines interior + boundary parts in fixed order, the communicator sums
+// over ranks (ncclAllReduce / thread group), and a one-thread kernel runs
+// the epilogue's finish() on the global totals, so the scalar recurrence
+// advances identically on every rank.
+template <int NV>
+__global__ void combine_kernel(double* base, int has_a, int has_b)
+{
+    const int i = threadIdx.x;
+    if (i < NV) {
+        double v = 0.0;
+        if (has_a) v = add_rn(v, base[i]);
+        if (has_b) v = add_rn(v, base[8 + i]);
+        base[16 + i] = v;
+    }
+}
+
+template <class E>
+__global__ void finish_kernel(E e, const double* tot)
+{
+    if (e.skip()) return;
+    double t[E::NV > 0 ? E::NV : 1];
+#pragma unroll
+    for (int i = 0; i < E::NV; ++i) t[i] = tot[i];
+    e.finish(t);
+}
+
+struct DistEnv {
+    lbk_ctx ctx;
+    lbk_dist_csr_s* D;
+    Comm* comm;
+    RedWs ws;
+    long long n_local() const { return D->n_local; }
+    long long n_ext() const { return static_cast<long long>(D->n_local) + D->n_ghost; }
+    long long n_global() const { return D->n_global; }
+    long long nnz_global() const { return D->nnz_global; }
+    bool ext_x() const { return true; }
+    bool multi() const { return comm && comm->nranks > 1; }
+
+    template <class E>
+    void finish(const E& e, int has_a, int has_b)
+    {
+        combine_kernel<E::NV><<<1, 32, 0, ctx->stream>>>(ws.out, has_a, has_b);
+        LBK_LAUNCH_CHECK();
+        if (multi()) comm->allreduce_sum(ws.out + 16, E::NV, ctx->stream);
+        finish_kernel<E><<<1, 1, 0, ctx->stream>>>(e, ws.out + 16);
+        LBK_LAUNCH_CHECK();
+    }
+    template <class Epi>
+    void apply(double* x, const Epi& e)
+    {
+        RedWs wa = ws, wb = ws;
+        wa.defer = wb.defer = 1;
+        wb.out = ws.out + 8;
+        dist_apply(ctx, D, comm, x, e, wa, wb);
+        finish(e, D->interior.nrows > 0, D->boundary.nrows > 0);
+    }
+    template <class Op>
+    void vec(const Op& o)
+    {
+        RedWs wa = ws;
+        wa.defer = 1;
+        launch_vec(ctx, D->n_local, o, wa);
+        finish(o, 1, 0);
+    }
+    double norm(const double* b)
+    {
+        double* d = ws.out + 24;
+        if (lbk_dot_f64_dev(ctx, D->n_local, b, b, d) != LBK_OK) fail(LBK_CUDA_ERROR, ctx->err);
+        if (multi()) comm->allreduce_sum(d, 1, ctx->stream);
+        double v = 0.0;
+        LBK_CUDA(cudaMemcpyAsync(&v, d, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        LBK_CUDA(cudaStreamSynchronize(ctx->stream));
+        return std::sqrt(v);
+    }
+};
+
+template <class Env>
+void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lbk_solver_cfg* cfg,
+                lbk_solve_result* res, double* history, int hist_cap)
 {
     // krylov.cpp:449-472 validation
     need(cfg != nullptr && res != nullptr, LBK_USAGE_ERROR, "solve: null config/result");
@@ -570,6 +674,7 @@ void solve_impl(lbk_ctx ctx, const Op& op, long long n, long long nnz, const dou
     const int limit = fixed ? cfg->fixed_iters : cfg->max_iters;
     const bool bicg = cfg->kind == 1;
     const bool recurrence = cfg->residual_mode == 1;
+    const long long n = env.n_local(), ne = env.n_ext();
 
     cudaEvent_t ev0, ev1;
     LBK_CUDA(cudaEventCreate(&ev0));
@@ -580,21 +685,19 @@ void solve_impl(lbk_ctx ctx, const Op& op, long long n, long long nnz, const dou
     auto* st = bufs.get<SolverState>(1);
     auto* hist = bufs.get<double>(size_t(limit) + 2);
     // norm_b (krylov.cpp:478) -- host value needed for the zero-b rule
-    double norm_b = 0.0;
-    if (lbk_nrm2_f64(ctx, n, b, &norm_b) != LBK_OK) fail(LBK_CUDA_ERROR, ctx->err);
-    RedWs ws = red_ws(ctx, kRedMaxBlocks, 2);
+    const double norm_b = env.norm(b);
     SolverState h{};
     h.limit = limit;
     h.fixed = fixed ? 1 : 0;
     h.tol = cfg->rel_tol;
     h.norm_b = norm_b;
-    h.n = n;
-    h.nnz = nnz;
-    h.flops = 2 * n;
+    h.n = env.n_global();
+    h.nnz = env.nnz_global();
+    h.flops = 2 * h.n;
     h.hist = hist;
     if (norm_b == 0.0) {
         // krylov.cpp:479-482: x = 0, converged, history [0]
-        LBK_CUDA(cudaMemsetAsync(x, 0, size_t(n) * sizeof(double), ctx->stream));
+        if (n) LBK_CUDA(cudaMemsetAsync(x_user, 0, size_t(n) * sizeof(double), ctx->stream));
         LBK_CUDA(cudaEventRecord(ev1, ctx->stream));
         LBK_CUDA(cudaEventSynchronize(ev1));
         float ms = 0;
@@ -603,7 +706,7 @@ void solve_impl(lbk_ctx ctx, const Op& op, long long n, long long nnz, const dou
         res->iterations = 0;
         res->final_rel_residual = 0.0;
         res->history_len = 1;
-        res->flop_count = 2 * n;
+        res->flop_count = 2 * h.n;
         res->elapsed = ms * 1e-3;
         if (history && hist_cap > 0) history[0] = 0.0;
         cudaEventDestroy(ev0);
@@ -612,14 +715,21 @@ void solve_impl(lbk_ctx ctx, const Op& op, long long n, long long nnz, const dou
     }
     LBK_CUDA(cudaMemcpyAsync(st, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
 
+    // vectors the operator is applied to (p, s, x) carry room for the halo
+    double* x = x_user;
+    if (env.ext_x()) {
+        x = bufs.get<double>(ne);
+        if (n) LBK_CUDA(cudaMemcpyAsync(x, x_user, size_t(n) * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, ctx->stream));
+    }
     double* r = bufs.get<double>(n);
-    double* p = bufs.get<double>(n);
+    double* p = bufs.get<double>(ne);
     double* q = bufs.get<double>(n);  // CG q / BiCGSTAB v
     double* rt = bicg ? bufs.get<double>(n) : nullptr;
-    double* s = bicg ? bufs.get<double>(n) : nullptr;
+    double* s = bicg ? bufs.get<double>(ne) : nullptr;
     double* t = bicg ? bufs.get<double>(n) : nullptr;
 
-    op.apply(ctx, x, EpiInit{b, r, p, rt, st, bicg ? 1 : 0}, ws);
+    env.apply(x, EpiInit{b, r, p, rt, st, bicg ? 1 : 0});
 
     // chunked launch loop; `done` is polled once per chunk
     int* done_host = reinterpret_cast<int*>(ctx->host_pinned);
@@ -628,20 +738,20 @@ void solve_impl(lbk_ctx ctx, const Op& op, long long n, long long nnz, const dou
     for (;;) {
         for (int c = 0; c < chunk && launched < limit; ++c, ++launched) {
             if (!bicg) {
-                op.apply(ctx, p, EpiCgK1{q, p, st}, ws);
-                launch_vec(ctx, n, OpCgK2{x, r, p, q, st, recurrence ? 1 : 0, 0.0}, ws);
+                env.apply(p, EpiCgK1{q, p, st});
+                env.vec(OpCgK2{x, r, p, q, st, recurrence ? 1 : 0, 0.0});
                 if (!recurrence) {
-                    op.apply(ctx, x, EpiCgK3{b, p, r, st}, ws);
+                    env.apply(x, EpiCgK3{b, p, r, st});
                 } else {
-                    op.apply(ctx, x, EpiTrueRes{b, st}, ws);
-                    launch_vec(ctx, n, OpCgP{p, r, st, 0.0}, ws);
+                    env.apply(x, EpiTrueRes{b, st});
+                    env.vec(OpCgP{p, r, st, 0.0});
                 }
             } else {
-                op.apply(ctx, p, EpiBiB2{q, rt, st}, ws);
-                launch_vec(ctx, n, OpBiB3{s, r, q, st, 0.0}, ws);
-                op.apply(ctx, s, EpiBiB4{t, s, st}, ws);
-                launch_vec(ctx, n, OpBiB5{x, r, p, s, t, rt, st, 0.0, 0.0}, ws);
-                op.apply(ctx, x, EpiBiB6{b, p, q, r, st}, ws);
+                env.apply(p, EpiBiB2{q, rt, st});
+                env.vec(OpBiB3{s, r, q, st, 0.0});
+                env.apply(s, EpiBiB4{t, s, st});
+                env.vec(OpBiB5{x, r, p, s, t, rt, st, 0.0, 0.0});
+                env.apply(x, EpiBiB6{b, p, q, r, st});
             }
         }
         LBK_CUDA(cudaMemcpyAsync(done_host, &st->done, sizeof(int), cudaMemcpyDeviceToHost,
@@ -649,6 +759,9 @@ void solve_impl(lbk_ctx ctx, const Op& op, long long n, long long nnz, const dou
         LBK_CUDA(cudaStreamSynchronize(ctx->stream));
         if (*done_host || launched >= limit) break;
     }
+    if (env.ext_x() && n)
+        LBK_CUDA(cudaMemcpyAsync(x_user, x, size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
     LBK_CUDA(cudaEventRecord(ev1, ctx->stream));
     LBK_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     LBK_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -708,7 +821,8 @@ lbk_status lbk_solve_csr(lbk_ctx ctx, const lbk_csr* A, const double* b, double*
             csr_plan_launch(ctx, A->row_ptr, A->nrows, A->nnz, plan);
             op.A.tile_rows = plan;
         }
-        solve_impl(ctx, op, A->nrows, A->nnz, b, x, cfg, result, history, history_cap);
+        LocalEnv<CsrOp> env{ctx, op, red_ws(ctx, kRedMaxBlocks, 2), A->nrows, A->nnz};
+        solve_impl(ctx, env, b, x, cfg, result, history, history_cap);
     });
 }
 
@@ -731,7 +845,21 @@ lbk_status lbk_solve_coo(lbk_ctx ctx, const lbk_coo* A, const double* b, double*
             coo_plan_launch(ctx, A->row_idx, A->nrows, A->nnz, plan);
             op.A.tile_starts = plan;
         }
-        solve_impl(ctx, op, A->nrows, A->nnz, b, x, cfg, result, history, history_cap);
+        LocalEnv<CooOp> env{ctx, op, red_ws(ctx, kRedMaxBlocks, 2), A->nrows, A->nnz};
+        solve_impl(ctx, env, b, x, cfg, result, history, history_cap);
+    });
+}
+
+lbk_status lbk_dist_solve(lbk_ctx ctx, lbk_dist_csr D, lbk_comm comm, const double* b, double* x,
+                          const lbk_solver_cfg* cfg, lbk_solve_result* result, double* history,
+                          int32_t history_cap)
+{
+    if (!ctx || !D) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        need(D->P == 1 || (comm && comm->impl->nranks == D->P && comm->impl->rank == D->rank),
+             LBK_USAGE_ERROR, "dist solve: communicator does not match the partition");
+        DistEnv env{ctx, D, comm ? comm->impl : nullptr, red_ws(ctx, kRedMaxBlocks, 2)};
+        solve_impl(ctx, env, b, x, cfg, result, history, history_cap);
     });
 }
 

@@ -111,12 +111,13 @@ class CudaExecutor:
     synchronize(), describe(), and an arena capacity whose excess raises
     OutOfMemoryError (executor.cpp:254-265)."""
 
-    def __init__(self, device: int = 0, arena_capacity: Optional[int] = None):
+    def __init__(self, device: int = 0, arena_capacity: Optional[int] = None,
+                 stream: Optional["torch.cuda.Stream"] = None):
         if not torch.cuda.is_available():
             raise DispatchError("CudaExecutor needs a CUDA device (no CPU fallback)")
         self.device = torch.device("cuda", device)
         self.lib = L.load()
-        stream = torch.cuda.current_stream(self.device)
+        stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         ctx = C.c_void_p()
         _check(self.lib.lbk_ctx_create_on_stream(device, C.c_void_p(stream.cuda_stream), C.byref(ctx)))
         self.ctx = ctx
