@@ -219,29 +219,16 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_s = float(e2e_t.item())
 
-    # ---- CG iterations/s (cfg4), replica per rank
+    # ---- CG iterations/s (cfg4): fused single-GPU solver at N = 1, the
+    # row-partitioned solver over NCCL (halo exchange + allreduce) at N > 1
     cg = None
     if not args.no_cg:
         del A, desc
         torch.cuda.empty_cache()
-        A4 = gen.stencil(ex, "7pt", 256)
-        ones = lk.vector_from(ex, np.ones(A4.ncols))
-        b = lk.make_vector(ex, A4.nrows)
-        lk.spmv(A4, ones, b)  # b = A*1 (harness.cpp:376-378); rows <= 32 -> bit-exact
-        cg = {"config": "cfg4: 7-pt Poisson 256^3, b = A*1, x0 = 0, tol 1e-8"}
-        for mode in ("true", "recurrence"):
-            xs = lk.zeros(ex, A4.nrows)
-            r = lk.solve(A4, b, xs, lk.SolverConfig(kind="cg", rel_tol=1e-8, max_iters=20000,
-                                                      residual_mode=mode))
-            tt = torch.tensor([r.elapsed], dtype=torch.float64, device=dev)
-            if world > 1:
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            el = float(tt.item())
-            cg[mode] = {"iterations": r.iterations, "golden_iterations": 581,
-                        "final_rel_residual": r.final_rel_residual, "seconds": el,
-                        "iters_per_s": world * r.iterations / el,
-                        "gflops_ref_model": world * r.flop_count / el / 1e9}
-        del A4, ones, b, xs
+        try:
+            cg = run_cg(ex, world, rank, local_rank, args.cg_dist)
+        except Exception as e:  # reported in the line, never fatal for the SpMV metric
+            cg = {"error": f"{type(e).__name__}: {e}"}
     clocks = sampler.stop()
 
     if rank != 0:
@@ -275,6 +262,71 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample()
     print(json.dumps(line), flush=True)
+
+
+def run_cg(ex, world: int, rank: int, local_rank: int, force_dist: bool = False) -> dict:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2011_08879_b200 import dist as D, gen, larch as lk
+
+    dev = ex.device
+    A4 = gen.stencil(ex, "7pt", 256)
+    n, nnz = A4.nrows, A4.nnz()
+    ones = lk.vector_from(ex, np.ones(A4.ncols))
+    b = lk.make_vector(ex, n)
+    lk.spmv(A4, ones, b)  # b = A*1 (harness.cpp:376-378); rows <= 32 -> bit-exact
+    cg = {"config": "cfg4: 7-pt Poisson 256^3, b = A*1, x0 = 0, tol 1e-8",
+          "golden_iterations": 581}
+
+    def tmax(v: float) -> float:
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    if world == 1 and not force_dist:
+        cg["mode"] = "single GPU, fused device-resident solver"
+        for mode in ("true", "recurrence"):
+            xs = lk.zeros(ex, n)
+            r = lk.solve(A4, b, xs, lk.SolverConfig(kind="cg", rel_tol=1e-8, max_iters=20000,
+                                                     residual_mode=mode))
+            cg[mode] = {"iterations": r.iterations, "final_rel_residual": r.final_rel_residual,
+                        "seconds": r.elapsed, "iters_per_s": r.iterations / r.elapsed,
+                        "gflops_ref_model": r.flop_count / r.elapsed / 1e9}
+        return cg
+    # distributed: this rank's rows of the same matrix
+    lo, hi = D.part_range(n, world, rank)
+    rp = A4.row_ptr[lo:hi + 1].cpu().numpy().astype(np.int64)
+    k0, k1 = int(rp[0]), int(rp[-1])
+    cols = A4.col_idx[k0:k1].cpu().numpy()
+    vals = A4.vals[k0:k1].cpu().numpy()
+    b_loc = b.values[lo:hi].clone()
+    del A4, ones, b
+    torch.cuda.empty_cache()
+    rp = (rp - k0).astype(np.int32)
+    m = D.DistMap(n, world, rank, rp, cols)
+    if world > 1:
+        D.exchange_requests(m)
+        comm = D.Communicator.nccl(local_rank)
+    else:  # --cg-dist at N = 1: the same path on a one-rank NCCL communicator
+        D.exchange_requests_local([m])
+        comm = D.Communicator.nccl_single(local_rank)
+    M = D.DistCsrMatrix(ex, m, rp, vals, nnz)
+    cg["mode"] = (f"row-partitioned over {world} GPUs: NCCL halo exchange overlapped with the "
+                  f"interior rows, ncclAllReduce per reduction (strong scaling)")
+    cg["n_ghost_rank0"] = M.n_ghost
+    for mode in ("true", "recurrence"):
+        x = torch.zeros(M.n_local, dtype=torch.float64, device=dev)
+        torch.cuda.synchronize()
+        r = M.solve(comm, b_loc, x, lk.SolverConfig(kind="cg", rel_tol=1e-8, max_iters=20000,
+                                                     residual_mode=mode))
+        el = tmax(r.elapsed)
+        cg[mode] = {"iterations": r.iterations, "final_rel_residual": r.final_rel_residual,
+                    "seconds": el, "iters_per_s": r.iterations / el,
+                    "gflops_ref_model": r.flop_count / el / 1e9}
+    return cg
 
 
 # ------------------------------------------------------------ CPU legs
@@ -342,6 +394,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cg", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cg-dist", action="store_true",
+                    help="use the row-partitioned solver for the CG leg even at N = 1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
