@@ -87,7 +87,20 @@ struct MappedEpi {
     static constexpr int NV = Epi::NV;
     Epi e;
     const int* __restrict__ map;
+    struct Pre {
+        int r;
+        typename EpiPre<Epi>::type p;
+    };
     __device__ bool skip() const { return e.skip(); }
+    __device__ Pre pre(int r) const
+    {
+        const int m = __ldg(map + r);
+        return {m, EpiPre<Epi>::load(e, m)};
+    }
+    __device__ void row_pre(int, double s, const Pre& p, double* acc) const
+    {
+        EpiPre<Epi>::row(e, p.r, s, p.p, acc);
+    }
     __device__ void row(int r, double s, double* acc) const { e.row(__ldg(map + r), s, acc); }
     __device__ void finish(const double* t) const { e.finish(t); }
 };

@@ -94,10 +94,15 @@ struct EpiInit {
     double* __restrict__ rt;  // may be null
     SolverState* st;
     int bicg;
+    struct Pre {
+        double b;
+    };
     __device__ bool skip() const { return false; }
-    __device__ void row(int i, double s, double* acc) const
+    __device__ Pre pre(int i) const { return {b[i]}; }
+    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
     {
-        const double v = add_rn(b[i], -s);
+        const double v = add_rn(pr.b, -s);
         r[i] = v;
         p[i] = v;
         if (rt) rt[i] = v;
@@ -137,11 +142,16 @@ struct EpiCgK1 {
     double* __restrict__ q;
     const double* __restrict__ p;
     SolverState* st;
+    struct Pre {
+        double p;
+    };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
-    __device__ void row(int i, double s, double* acc) const
+    __device__ Pre pre(int i) const { return {p[i]}; }
+    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
     {
         q[i] = s;
-        acc[0] = add_rn(acc[0], mul_rn(p[i], s));
+        acc[0] = add_rn(acc[0], mul_rn(pr.p, s));
     }
     __device__ void finish(const double* tot) const
     {
@@ -164,13 +174,18 @@ struct EpiCgK3 {
     double* __restrict__ p;
     const double* __restrict__ r;
     SolverState* st;
+    struct Pre {
+        double b, p, r;
+    };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
-    __device__ void row(int i, double s, double* acc) const
+    __device__ Pre pre(int i) const { return {b[i], p[i], r[i]}; }
+    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
     {
-        const double t = add_rn(b[i], -s);
+        const double t = add_rn(pr.b, -s);
         acc[0] = add_rn(acc[0], mul_rn(t, t));
         const double beta = st->beta;
-        p[i] = add_rn(mul_rn(p[i], beta), r[i]);
+        p[i] = add_rn(mul_rn(pr.p, beta), pr.r);
     }
     __device__ void finish(const double* tot) const;
 };
@@ -213,10 +228,15 @@ struct EpiTrueRes {
     static constexpr int NV = 1;
     const double* __restrict__ b;
     SolverState* st;
+    struct Pre {
+        double b;
+    };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0 || !st->verify_pending; }
-    __device__ void row(int i, double s, double* acc) const
+    __device__ Pre pre(int i) const { return {b[i]}; }
+    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int, double s, const Pre& pr, double* acc) const
     {
-        const double t = add_rn(b[i], -s);
+        const double t = add_rn(pr.b, -s);
         acc[0] = add_rn(acc[0], mul_rn(t, t));
     }
     __device__ void finish(const double* tot) const
@@ -252,11 +272,16 @@ struct EpiBiB2 {
     double* __restrict__ v;
     const double* __restrict__ rt;
     SolverState* st;
+    struct Pre {
+        double rt;
+    };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
-    __device__ void row(int i, double s, double* acc) const
+    __device__ Pre pre(int i) const { return {rt[i]}; }
+    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
     {
         v[i] = s;
-        acc[0] = add_rn(acc[0], mul_rn(rt[i], s));
+        acc[0] = add_rn(acc[0], mul_rn(pr.rt, s));
     }
     __device__ void finish(const double* tot) const
     {
@@ -276,12 +301,17 @@ struct EpiBiB4 {
     double* __restrict__ t;
     const double* __restrict__ s;
     SolverState* st;
+    struct Pre {
+        double s;
+    };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
-    __device__ void row(int i, double sum, double* acc) const
+    __device__ Pre pre(int i) const { return {s[i]}; }
+    __device__ void row(int i, double sum, double* acc) const { row_pre(i, sum, pre(i), acc); }
+    __device__ void row_pre(int i, double sum, const Pre& pr, double* acc) const
     {
         t[i] = sum;
         acc[0] = add_rn(acc[0], mul_rn(sum, sum));
-        acc[1] = add_rn(acc[1], mul_rn(sum, s[i]));
+        acc[1] = add_rn(acc[1], mul_rn(sum, pr.s));
     }
     __device__ void finish(const double* tot) const
     {
@@ -308,13 +338,18 @@ struct EpiBiB6 {
     const double* __restrict__ v;
     const double* __restrict__ r;
     SolverState* st;
+    struct Pre {
+        double b, p, v, r;
+    };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
-    __device__ void row(int i, double s, double* acc) const
+    __device__ Pre pre(int i) const { return {b[i], p[i], v[i], r[i]}; }
+    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
     {
-        const double t = add_rn(b[i], -s);
+        const double t = add_rn(pr.b, -s);
         acc[0] = add_rn(acc[0], mul_rn(t, t));
         const double beta = st->beta, omega = st->omega;
-        p[i] = add_rn(mul_rn(add_rn(p[i], mul_rn(-omega, v[i])), beta), r[i]);
+        p[i] = add_rn(mul_rn(add_rn(pr.p, mul_rn(-omega, pr.v)), beta), pr.r);
     }
     __device__ void finish(const double* tot) const
     {

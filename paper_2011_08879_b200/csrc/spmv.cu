@@ -46,7 +46,7 @@ void csr_plan_launch(lbk_ctx ctx, const int* row_ptr, int nrows, long long nnz, 
 {
     const int nt = csr_ntiles(nnz, nrows);
     csr_plan_kernel<<<ceil_div(nt + 1, 256), 256, 0, ctx->stream>>>(
-        row_ptr, nrows, nt, stream_tile_nnz(nnz, nrows), tile_rows);
+        row_ptr, nrows, nt, stream_tile_nnz(nnz, nrows, 1), tile_rows);
     LBK_LAUNCH_CHECK();
 }
 
@@ -54,7 +54,7 @@ void coo_plan_launch(lbk_ctx ctx, const int* rows, int nrows, long long nnz, int
 {
     const int nt = coo_ntiles(nnz, nrows);
     coo_plan_kernel<<<ceil_div(nt + 1, 256), 256, 0, ctx->stream>>>(
-        rows, nnz, nt, stream_tile_nnz(nnz, nrows), tile_starts);
+        rows, nnz, nt, stream_tile_nnz(nnz, nrows, 2), tile_starts);
     LBK_LAUNCH_CHECK();
 }
 

@@ -18,6 +18,8 @@
 //     dot products / vector updates into the SpMV pass (solver.cu).
 #pragma once
 
+#include <type_traits>
+
 #include "lbk_internal.cuh"
 
 namespace lbk {
@@ -80,13 +82,18 @@ struct EpiAxpby {
     static constexpr int NV = 0;
     T* __restrict__ y;
     T alpha, beta;
+    struct Pre {
+        T y;
+    };
     __device__ bool skip() const { return false; }
-    __device__ void row(int r, T s, double*) const
+    __device__ Pre pre(int r) const { return {beta != T(0) ? y[r] : T(0)}; }
+    __device__ void row_pre(int r, T s, const Pre& p, double*) const
     {
         T v = mul_rn(alpha, s);
-        if (beta != T(0)) v = add_rn(v, mul_rn(beta, y[r]));
+        if (beta != T(0)) v = add_rn(v, mul_rn(beta, p.y));
         y[r] = v;
     }
+    __device__ void row(int r, T s, double* acc) const { row_pre(r, s, pre(r), acc); }
     __device__ void finish(const double*) const {}
 };
 
@@ -127,18 +134,20 @@ template <typename T>
 struct StreamCfg {
     static constexpr int kWarps = 4;                 // warps per CTA
     static constexpr int kThreads = kWarps * 32;
-    static constexpr int kCap = 1024;                // entries per slot
+    // entries per slot: COO stages 16 B/entry, so its slots are smaller to
+    // keep two 4-warp CTAs (8 pipelines) resident per SM
+    static constexpr int cap(int idx_arrays) { return idx_arrays == 1 ? 1024 : 768; }
         static constexpr int kIdxArrays = 1;             // CSR: col_idx
     static constexpr size_t slot_bytes(int idx_arrays)
     {
-        return size_t(kCap) * (sizeof(T) + 4 * idx_arrays);
+        return size_t(cap(idx_arrays)) * (sizeof(T) + 4 * idx_arrays);
     }
     static constexpr size_t smem_bytes(int idx_arrays)
     {
         return size_t(kWarps) * 2 * slot_bytes(idx_arrays);
     }
 };
-constexpr int kTileMin = 384, kTileMax = 896;
+constexpr int kTileMin = 384;
 
 // Rows per lane per pass (G) from the mean row length: G*CH = 32 gathers
 // in flight per lane whichever the row length.
@@ -151,11 +160,12 @@ inline int stream_group(long long nnz, long long nrows)
 // nnz-balanced tile size: one pass of the warp (32*G rows of mean length),
 // clamped so the tile plus a straddling row and alignment padding fits a
 // slot.
-inline long long stream_tile_nnz(long long nnz, long long nrows)
+inline long long stream_tile_nnz(long long nnz, long long nrows, int idx_arrays)
 {
+    const long long tmax = StreamCfg<double>::cap(idx_arrays) - 128;
     long long mean = nrows > 0 ? (nnz + nrows - 1) / nrows : 1;
     long long t = 32LL * stream_group(nnz, nrows) * (mean < 1 ? 1 : mean);
-    t = t < kTileMin ? kTileMin : (t > kTileMax ? kTileMax : t);
+    t = t < kTileMin ? kTileMin : (t > tmax ? tmax : t);
     return t;
 }
 
@@ -201,38 +211,73 @@ __device__ __forceinline__ T warp_row_global(int ks, int ke, const int* __restri
     return warp_sum(add_rn(add_rn(p0, p1), add_rn(p2, p3)));
 }
 
+// Epilogue operand prefetch: an epilogue may declare `struct Pre`, `Pre
+// pre(int r)` and `row_pre(r, s, pre, acc)`; the staged sweep then issues
+// the row's operand loads (b[r], p[r], ...) together with its gathers, so
+// one memory round trip per pass serves both.
+template <class Epi, class = void>
+struct EpiPre {
+    struct type {};
+    __device__ static type load(const Epi&, int) { return {}; }
+    template <typename T>
+    __device__ static void row(const Epi& e, int r, T s, const type&, double* acc)
+    {
+        e.row(r, s, acc);
+    }
+};
+template <class Epi>
+struct EpiPre<Epi, std::void_t<typename Epi::Pre>> {
+    using type = typename Epi::Pre;
+    __device__ static type load(const Epi& e, int r) { return e.pre(r); }
+    template <typename T>
+    __device__ static void row(const Epi& e, int r, T s, const type& p, double* acc)
+    {
+        e.row_pre(r, s, p, acc);
+    }
+};
+
+constexpr int kSeqRow = 256;  // staged rows up to this length stay bit-exact
+
 // Phase B of a staged tile, lane-per-row.  A lane owns G rows per pass
 // (rows base + g*32 + lane) and gathers the first CH entries of each of them
 // before summing, so G*CH (= 32) independent gathers per lane are in flight
-// per pass; rows with CH < len <= kLongRow continue lane-privately, longer
-// rows are reduced by the whole warp.  Every row is summed sequentially from
-// 0.0 in ascending k with individually rounded products.
-template <typename T, int G, class Epi, class Ext>
-__device__ __forceinline__ void staged_rows(int rb, int re, const T* sv, const int* sc,
+// per pass, together with the epilogue's operand loads.  Longer rows are
+// batched: the warp
+// computes the products of all of them in place (entry-parallel, 8 gathers
+// per lane in flight), then each is summed sequentially by its own lane
+// (len <= kSeqRow) or reduced by the warp.  Every row of <= kSeqRow entries
+// is summed sequentially from 0.0 in ascending k with individually rounded
+// products -- the reference's bits.  `first(q)` gives the extents of the
+// first pass (prefetched by the tile loop), `extent(r)` any row's.
+template <typename T, int G, class Epi, class First, class Ext>
+__device__ __forceinline__ void staged_rows(int rb, int re, T* sv, const int* sc,
                                             const T* __restrict__ x, const Epi& epi,
-                                            double* acc, Ext&& extent)
+                                            double* acc, First&& first, Ext&& extent)
 {
+    using EP = EpiPre<Epi>;
     constexpr int CH = 32 / G;
     const int lane = threadIdx.x & 31;
     for (int base = rb; base < re; base += 32 * G) {
         int o[G], len[G];
         T v[G][CH], g[G][CH];
+        typename EP::type pre[G];
         unsigned lm = 0;
 #pragma unroll
         for (int q = 0; q < G; ++q) {
             const int r = base + q * 32 + lane;
-            int2 e = make_int2(0, 0);
-            if (r < re) e = extent(r);
+            int2 e = base == rb ? first(q) : make_int2(0, 0);
+            if (base != rb && r < re) e = extent(r);
+            if (r >= re) e = make_int2(0, 0);
             o[q] = e.x;
             len[q] = e.y;
-            lm |= __ballot_sync(0xffffffffu, e.y > kLongRow) != 0 ? (1u << q) : 0u;
-            if (e.y > kLongRow) len[q] = -1;  // warp-cooperative below
+            lm |= __ballot_sync(0xffffffffu, e.y > CH) != 0 ? (1u << q) : 0u;
+            if (r < re) pre[q] = EP::load(epi, r);
         }
 #pragma unroll
         for (int q = 0; q < G; ++q) {
 #pragma unroll
             for (int j = 0; j < CH; ++j) {
-                if (j < len[q]) {
+                if (j < len[q] && len[q] <= CH) {
                     v[q][j] = sv[o[q] + j];
                     g[q][j] = ldg_nc(x + sc[o[q] + j]);
                 }
@@ -241,31 +286,72 @@ __device__ __forceinline__ void staged_rows(int rb, int re, const T* sv, const i
 #pragma unroll
         for (int q = 0; q < G; ++q) {
             const int r = base + q * 32 + lane;
-            if (r < re && len[q] >= 0) {
+            if (r < re && len[q] <= CH) {
                 T sum = T(0);
 #pragma unroll
                 for (int j = 0; j < CH; ++j)
                     if (j < len[q]) sum = add_rn(sum, mul_rn(v[q][j], g[q][j]));
-                for (int j = CH; j < len[q]; ++j)
-                    sum = add_rn(sum, mul_rn(sv[o[q] + j], ldg_nc(x + sc[o[q] + j])));
-                epi.row(r, sum, acc);
+                EP::row(epi, r, sum, pre[q], acc);
             }
         }
 #pragma unroll
         for (int q = 0; q < G; ++q) {
             if (!(lm & (1u << q))) continue;
-            unsigned m = __ballot_sync(0xffffffffu, len[q] < 0 && base + q * 32 + lane < re);
+            const int r = base + q * 32 + lane;
+            const bool lng = r < re && len[q] > CH;
+            // exclusive prefix of the long rows' lengths over the lanes
+            int L = lng ? len[q] : 0, inc = L;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += t;
+            }
+            const int total = __shfl_sync(0xffffffffu, inc, 31);
+            // products of every long entry, in place, 8 gathers per lane in flight
+            for (int e0 = 0; e0 < total; e0 += 256) {
+                int pos[8];
+                T gv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = e0 + u * 32 + lane;
+                    pos[u] = -1;
+                    // owner lane: first lane whose inclusive prefix exceeds e
+                    int lo = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const int t = __shfl_sync(0xffffffffu, inc, lo + step - 1);
+                        if (t <= e) lo += step;
+                    }
+                    const int own_inc = __shfl_sync(0xffffffffu, inc, lo);
+                    const int own_len = __shfl_sync(0xffffffffu, L, lo);
+                    const int own_o = __shfl_sync(0xffffffffu, o[q], lo);
+                    if (e < total) {
+                        pos[u] = own_o + (e - (own_inc - own_len));
+                        gv[u] = ldg_nc(x + sc[pos[u]]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (pos[u] >= 0) sv[pos[u]] = mul_rn(sv[pos[u]], gv[u]);
+            }
+            __syncwarp();
+            if (lng && L <= kSeqRow) {
+                T sum = T(0);
+                for (int k = 0; k < L; ++k) sum = add_rn(sum, sv[o[q] + k]);
+                EP::row(epi, r, sum, pre[q], acc);
+            }
+            unsigned m = __ballot_sync(0xffffffffu, lng && L > kSeqRow);
             while (m) {
                 const int src = __ffs(m) - 1;
                 m &= m - 1;
-                const int rr = base + q * 32 + src;
-                const int2 e = extent(rr);
+                const int ss = __shfl_sync(0xffffffffu, o[q], src);
+                const int ll = __shfl_sync(0xffffffffu, L, src);
                 T part = T(0);
-                for (int k = lane; k < e.y; k += 32)
-                    part = add_rn(part, mul_rn(sv[e.x + k], ldg_nc(x + sc[e.x + k])));
+                for (int k = lane; k < ll; k += 32) part = add_rn(part, sv[ss + k]);
                 part = warp_sum(part);
-                if (lane == 0) epi.row(rr, part, acc);
+                if (lane == src) EP::row(epi, r, part, pre[q], acc);
             }
+            __syncwarp();
         }
     }
 }
@@ -314,14 +400,17 @@ __device__ __forceinline__ int stage_tile(int k0, int k1, long long nnz4, T* sv,
 //                 stage T_{i+1} (bounds complete);  process T_i.
 // meta1(t) / meta2(t, m1) return the lane-0/1 values (lanes >= 2: 0);
 // mk(m1, m2) -> int4 (row begin, row end, entry begin, entry end).
-template <typename T, int NIDX, class M1, class M2, class Mk, class Staged, class Wide>
+// pf(bounds) issues per-lane loads for the first row pass of a tile (CSR:
+// its row_ptr entries) one tile ahead; staged(...) gets them back.
+template <typename T, int NIDX, class M1, class M2, class Mk, class Pf, class Staged, class Wide>
 __device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const T* vals,
                                                const int* idx0, const int* idx1,
                                                unsigned char* wbase, uint64_t* bar, M1&& meta1,
-                                               M2&& meta2, Mk&& mk, Staged&& staged, Wide&& wide)
+                                               M2&& meta2, Mk&& mk, Pf&& pf, Staged&& staged,
+                                               Wide&& wide)
 {
     using Cfg = StreamCfg<T>;
-    constexpr int CAP = Cfg::kCap, NW = Cfg::kWarps;
+    constexpr int CAP = Cfg::cap(NIDX), NW = Cfg::kWarps;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     T* sv[2];
     int *si0[2], *si1[2];
@@ -353,6 +442,7 @@ __device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const 
     if (st_cur)
         ka_cur = stage_tile<T, NIDX>(cur.z, cur.w, nnz4, sv[0], si0[0], si1[0], vals, idx0, idx1,
                                      &bar[0], pol);
+    auto pf_cur = pf(cur);
     for (int it = 0; t < ntiles; t += nw, ++it) {
         const int slot = it & 1;
         const int m1d = meta1(t + 3 * nw);     // consumed two iterations later
@@ -366,15 +456,17 @@ __device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const 
             ka_nxt = stage_tile<T, NIDX>(nxt.z, nxt.w, nnz4, sv[slot ^ 1], si0[slot ^ 1],
                                          si1[slot ^ 1], vals, idx0, idx1, &bar[slot ^ 1], pol);
         }
+        const auto pf_nxt = pf(has_nxt ? nxt : make_int4(0, 0, 0, 0));
         if (!st_cur && lane == 0) mbar_arrive(&bar[slot]);  // keep the phase in step
         mbar_wait(&bar[slot], (it >> 1) & 1);
         __syncwarp();
-        if (st_cur) staged(cur, ka_cur, sv[slot], si0[slot], si1[slot]);
+        if (st_cur) staged(cur, ka_cur, sv[slot], si0[slot], si1[slot], pf_cur);
         else wide(cur);
         __syncwarp();
         cur = nxt;
         st_cur = st_nxt;
         ka_cur = ka_nxt;
+        pf_cur = pf_nxt;
         m1b = m1c;
         m1c = m1d;
         m2b = m2c;
@@ -382,7 +474,7 @@ __device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const 
 }
 
 template <typename T, class Epi, int G>
-__global__ void __launch_bounds__(StreamCfg<T>::kThreads)
+__global__ void __launch_bounds__(StreamCfg<T>::kThreads, 2)
     csr_stream_kernel(CsrView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
 {
     using Cfg = StreamCfg<T>;
@@ -396,6 +488,9 @@ __global__ void __launch_bounds__(StreamCfg<T>::kThreads)
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc[i] = 0.0;
 
+    struct RowPf {
+        int v[G + 1];
+    };
     warp_tile_loop<T, 1>(
         A.ntiles, A.nnz, A.vals, A.cols, nullptr,
         smem + size_t(warp) * 2 * Cfg::slot_bytes(1), bars[warp],
@@ -405,11 +500,34 @@ __global__ void __launch_bounds__(StreamCfg<T>::kThreads)
             return make_int4(__shfl_sync(0xffffffffu, b, 0), __shfl_sync(0xffffffffu, b, 1),
                              __shfl_sync(0xffffffffu, k, 0), __shfl_sync(0xffffffffu, k, 1));
         },
-        [&](int4 bd, int ka, const T* sv, const int* sc, const int*) {
-            staged_rows<T, G>(bd.x, bd.y, sv, sc, x, epi, acc, [&](int r) {
-                const int rs = __ldg(A.row_ptr + r);
-                return make_int2(rs - ka, __ldg(A.row_ptr + r + 1) - rs);
-            });
+        [&](int4 bd) {
+            // row_ptr of the tile's first pass: lane holds rows rb + q*32 + lane
+            RowPf p;
+#pragma unroll
+            for (int q = 0; q <= G; ++q) {
+                const int r = bd.x + q * 32 + lane;
+                p.v[q] = __ldg(A.row_ptr + (r < bd.y ? r : bd.y));
+            }
+            return p;
+        },
+        [&](int4 bd, int ka, T* sv, const int* sc, const int*, const RowPf& p) {
+            staged_rows<T, G>(
+                bd.x, bd.y, sv, sc, x, epi, acc,
+                [&](int q) {
+                    // end of row (q, lane) = start held by lane + 1 (lane 31:
+                    // lane 0 of group q + 1)
+                    int nx = __shfl_sync(0xffffffffu, p.v[q], (lane + 1) & 31);
+                    int wrap = 0;
+#pragma unroll
+                    for (int u = 0; u <= G; ++u)
+                        if (u == q + 1) wrap = __shfl_sync(0xffffffffu, p.v[u], 0);
+                    if (lane == 31) nx = wrap;
+                    return make_int2(p.v[q] - ka, nx - p.v[q]);
+                },
+                [&](int r) {
+                    const int rs = __ldg(A.row_ptr + r);
+                    return make_int2(rs - ka, __ldg(A.row_ptr + r + 1) - rs);
+                });
         },
         [&](int4 bd) {
             for (int r = bd.x; r < bd.y; ++r) {
@@ -433,7 +551,7 @@ __global__ void __launch_bounds__(StreamCfg<T>::kThreads)
 // row_idx is staged with vals/col_idx; a lane finds its row's extent by
 // binary search over the staged row indices.
 template <typename T, class Epi, int G>
-__global__ void __launch_bounds__(StreamCfg<T>::kThreads)
+__global__ void __launch_bounds__(StreamCfg<T>::kThreads, 2)
     coo_stream_kernel(CooView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
 {
     using Cfg = StreamCfg<T>;
@@ -447,6 +565,7 @@ __global__ void __launch_bounds__(StreamCfg<T>::kThreads)
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc[i] = 0.0;
 
+    struct NoPf {};
     warp_tile_loop<T, 2>(
         A.ntiles, A.nnz, A.vals, A.cols, A.rows,
         smem + size_t(warp) * 2 * Cfg::slot_bytes(2), bars[warp],
@@ -460,12 +579,20 @@ __global__ void __launch_bounds__(StreamCfg<T>::kThreads)
             return make_int4(__shfl_sync(0xffffffffu, r, 0), __shfl_sync(0xffffffffu, r, 1),
                              __shfl_sync(0xffffffffu, k, 0), __shfl_sync(0xffffffffu, k, 1));
         },
-        [&](int4 bd, int ka, const T* sv, const int* sc, const int* sr) {
+        [&](int4) { return NoPf{}; },
+        [&](int4 bd, int ka, T* sv, const int* sc, const int* sr, const NoPf&) {
             const int lo = bd.z - ka, hi = bd.w - ka;
-            staged_rows<T, G>(bd.x, bd.y, sv, sc, x, epi, acc, [&](int r) {
+            auto ext = [&](int r) {
                 const int rs = lower_bound_i(sr, lo, hi, r);
                 return make_int2(rs, lower_bound_i(sr, rs, hi, r + 1) - rs);
-            });
+            };
+            staged_rows<T, G>(
+                bd.x, bd.y, sv, sc, x, epi, acc,
+                [&](int q) {
+                    const int r = bd.x + q * 32 + lane;
+                    return r < bd.y ? ext(r) : make_int2(0, 0);
+                },
+                ext);
         },
         [&](int4 bd) {
             for (int r = bd.x; r < bd.y; ++r) {

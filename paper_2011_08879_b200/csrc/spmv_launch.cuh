@@ -14,13 +14,14 @@ namespace lbk {
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // Number of plan tiles (the plan holds ntiles + 1 int32 boundaries).
-inline int csr_ntiles(long long nnz, long long nrows)
+inline int stream_ntiles(long long nnz, long long nrows, int idx_arrays)
 {
-    const long long tn = stream_tile_nnz(nnz, nrows);
+    const long long tn = stream_tile_nnz(nnz, nrows, idx_arrays);
     long long t = (nnz + tn - 1) / tn;
     return static_cast<int>(t < 1 ? 1 : t);
 }
-inline int coo_ntiles(long long nnz, long long nrows) { return csr_ntiles(nnz, nrows); }
+inline int csr_ntiles(long long nnz, long long nrows) { return stream_ntiles(nnz, nrows, 1); }
+inline int coo_ntiles(long long nnz, long long nrows) { return stream_ntiles(nnz, nrows, 2); }
 
 void csr_plan_launch(lbk_ctx ctx, const int* row_ptr, int nrows, long long nnz, int* tile_rows);
 void coo_plan_launch(lbk_ctx ctx, const int* rows, int nrows, long long nnz, int* tile_starts);
