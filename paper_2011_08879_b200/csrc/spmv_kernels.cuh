@@ -130,22 +130,37 @@ __global__ void coo_plan_kernel(const int* __restrict__ rows, long long nnz, int
 // Tiles wider than a slot go straight from global memory, warp per row.
 // The tile size is chosen per matrix (~32 rows of mean length, so one pass
 // of the warp covers the tile): see stream_tile_nnz().
-template <typename T>
+#ifndef LBK_CSR_CAP
+#define LBK_CSR_CAP 1024
+#endif
+#ifndef LBK_CSR_SLOTS
+#define LBK_CSR_SLOTS 2
+#endif
+#ifndef LBK_CSR_WARPS
+#define LBK_CSR_WARPS 4
+#endif
+#ifndef LBK_COO_CAP
+#define LBK_COO_CAP 768
+#endif
+#ifndef LBK_COO_SLOTS
+#define LBK_COO_SLOTS 2
+#endif
+#ifndef LBK_COO_WARPS
+#define LBK_COO_WARPS 4
+#endif
+// Per-format pipeline shape (measured on B200, scripts/variants.sh): a warp
+// keeps kSlots-1 tiles in flight while it sweeps one.  CSR: 2 slots x 12 KB
+// per warp, 4-warp CTAs, 2 CTAs (8 pipelines) per SM -- 3 slots with fewer
+// warps, or smaller slots with more warps, were both slower on cfg2 and
+// cfg4.  COO stages 16 B/entry: 2 slots x 12 KB (768 entries), 4-warp CTAs.
+template <typename T, int NIDX>
 struct StreamCfg {
-    static constexpr int kWarps = 4;                 // warps per CTA
+    static constexpr int kCap = NIDX == 1 ? LBK_CSR_CAP : LBK_COO_CAP;  // entries per slot
+    static constexpr int kSlots = NIDX == 1 ? LBK_CSR_SLOTS : LBK_COO_SLOTS;
+    static constexpr int kWarps = NIDX == 1 ? LBK_CSR_WARPS : LBK_COO_WARPS;
     static constexpr int kThreads = kWarps * 32;
-    // entries per slot: COO stages 16 B/entry, so its slots are smaller to
-    // keep two 4-warp CTAs (8 pipelines) resident per SM
-    static constexpr int cap(int idx_arrays) { return idx_arrays == 1 ? 1024 : 768; }
-        static constexpr int kIdxArrays = 1;             // CSR: col_idx
-    static constexpr size_t slot_bytes(int idx_arrays)
-    {
-        return size_t(cap(idx_arrays)) * (sizeof(T) + 4 * idx_arrays);
-    }
-    static constexpr size_t smem_bytes(int idx_arrays)
-    {
-        return size_t(kWarps) * 2 * slot_bytes(idx_arrays);
-    }
+    static constexpr size_t slot_bytes = size_t(kCap) * (sizeof(T) + 4 * NIDX);
+    static constexpr size_t smem_bytes = size_t(kWarps) * kSlots * slot_bytes;
 };
 constexpr int kTileMin = 384;
 
@@ -162,7 +177,8 @@ inline int stream_group(long long nnz, long long nrows)
 // slot.
 inline long long stream_tile_nnz(long long nnz, long long nrows, int idx_arrays)
 {
-    const long long tmax = StreamCfg<double>::cap(idx_arrays) - 128;
+    const long long tmax =
+        (idx_arrays == 1 ? StreamCfg<double, 1>::kCap : StreamCfg<double, 2>::kCap) - 128;
     long long mean = nrows > 0 ? (nnz + nrows - 1) / nrows : 1;
     long long t = 32LL * stream_group(nnz, nrows) * (mean < 1 ? 1 : mean);
     t = t < kTileMin ? kTileMin : (t > tmax ? tmax : t);
@@ -392,16 +408,18 @@ __device__ __forceinline__ int stage_tile(int k0, int k1, long long nnz4, T* sv,
     return ka;
 }
 
-// The per-warp tile loop shared by CSR and COO.  Tile metadata needs two
+// The per-warp tile loop shared by CSR and COO.  Tiles T_j = t0 + j*nw of
+// this warp rotate through NS shared-memory slots: at iteration j the warp
+// stages T_{j+NS-1} (bulk copies into the slot T_{j-1} just freed) and then
+// sweeps T_j, so NS-1 tiles are always in flight.  Tile metadata needs two
 // dependent loads (plan entry, then row_ptr / row_idx at it); they are
-// software-pipelined two and one tiles ahead so neither the bulk-copy issue
-// nor the row sweep ever waits on them:
-//   iteration i:  load m1(T_{i+3});  load m2(T_{i+2}) from m1(T_{i+2});
-//                 stage T_{i+1} (bounds complete);  process T_i.
+// software-pipelined two and one tiles ahead of the staging:
+//   iteration j:  load m1(T_{j+NS+1});  load m2(T_{j+NS}) from m1(T_{j+NS});
+//                 stage T_{j+NS-1} (bounds complete);  sweep T_j.
 // meta1(t) / meta2(t, m1) return the lane-0/1 values (lanes >= 2: 0);
 // mk(m1, m2) -> int4 (row begin, row end, entry begin, entry end).
 // pf(bounds) issues per-lane loads for the first row pass of a tile (CSR:
-// its row_ptr entries) one tile ahead; staged(...) gets them back.
+// its row_ptr entries) when the tile is staged; staged(...) gets them back.
 template <typename T, int NIDX, class M1, class M2, class Mk, class Pf, class Staged, class Wide>
 __device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const T* vals,
                                                const int* idx0, const int* idx1,
@@ -409,21 +427,15 @@ __device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const 
                                                M2&& meta2, Mk&& mk, Pf&& pf, Staged&& staged,
                                                Wide&& wide)
 {
-    using Cfg = StreamCfg<T>;
-    constexpr int CAP = Cfg::cap(NIDX), NW = Cfg::kWarps;
+    using Cfg = StreamCfg<T, NIDX>;
+    constexpr int CAP = Cfg::kCap, NW = Cfg::kWarps, NS = Cfg::kSlots;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    T* sv[2];
-    int *si0[2], *si1[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        unsigned char* b = wbase + q * Cfg::slot_bytes(NIDX);
-        sv[q] = reinterpret_cast<T*>(b);
-        si0[q] = reinterpret_cast<int*>(b + CAP * sizeof(T));
-        si1[q] = si0[q] + CAP;
-    }
+    auto slot_v = [&](int s) { return reinterpret_cast<T*>(wbase + s * Cfg::slot_bytes); };
+    auto slot_i0 = [&](int s) {
+        return reinterpret_cast<int*>(wbase + s * Cfg::slot_bytes + CAP * sizeof(T));
+    };
     if (lane == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int q = 0; q < NS; ++q) mbar_init(&bar[q], 1);
         fence_mbar_init();
     }
     __syncwarp();
@@ -432,55 +444,79 @@ __device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const 
     const int nw = gridDim.x * NW;
     auto staged_ok = [&](int4 bd) { return (bd.w - (bd.z & ~3) + 3) <= CAP; };
 
-    int t = blockIdx.x * NW + warp;
-    if (t >= ntiles) return;
-    int m1a = meta1(t), m1b = meta1(t + nw), m1c = meta1(t + 2 * nw);
-    int4 cur = mk(m1a, meta2(t, m1a));
-    int m2b = meta2(t + nw, m1b);
-    bool st_cur = staged_ok(cur);
-    int ka_cur = 0;
-    if (st_cur)
-        ka_cur = stage_tile<T, NIDX>(cur.z, cur.w, nnz4, sv[0], si0[0], si1[0], vals, idx0, idx1,
-                                     &bar[0], pol);
-    auto pf_cur = pf(cur);
-    for (int it = 0; t < ntiles; t += nw, ++it) {
-        const int slot = it & 1;
-        const int m1d = meta1(t + 3 * nw);     // consumed two iterations later
-        const int m2c = meta2(t + 2 * nw, m1c);  // consumed next iteration
-        const int4 nxt = mk(m1b, m2b);
-        const bool has_nxt = t + nw < ntiles;
-        const bool st_nxt = has_nxt && staged_ok(nxt);
-        int ka_nxt = 0;
-        if (st_nxt) {
+    const int t0 = blockIdx.x * NW + warp;
+    if (t0 >= ntiles) return;
+    using PfT = decltype(pf(make_int4(0, 0, 0, 0)));
+    struct Q {
+        int4 bd;
+        int ka;
+        bool st;
+        PfT pf;
+    };
+    // stage tile t (if it exists) into slot s
+    auto issue = [&](int t, int4 bd, int s) {
+        Q q;
+        q.bd = bd;
+        q.st = t < ntiles && staged_ok(bd);
+        q.ka = 0;
+        if (q.st) {
             fence_proxy_async_smem();
-            ka_nxt = stage_tile<T, NIDX>(nxt.z, nxt.w, nnz4, sv[slot ^ 1], si0[slot ^ 1],
-                                         si1[slot ^ 1], vals, idx0, idx1, &bar[slot ^ 1], pol);
+            int* i0 = slot_i0(s);
+            q.ka = stage_tile<T, NIDX>(bd.z, bd.w, nnz4, slot_v(s), i0, i0 + CAP, vals, idx0, idx1,
+                                       &bar[s], pol);
         }
-        const auto pf_nxt = pf(has_nxt ? nxt : make_int4(0, 0, 0, 0));
-        if (!st_cur && lane == 0) mbar_arrive(&bar[slot]);  // keep the phase in step
-        mbar_wait(&bar[slot], (it >> 1) & 1);
-        __syncwarp();
-        if (st_cur) staged(cur, ka_cur, sv[slot], si0[slot], si1[slot], pf_cur);
-        else wide(cur);
-        __syncwarp();
-        cur = nxt;
-        st_cur = st_nxt;
-        ka_cur = ka_nxt;
-        pf_cur = pf_nxt;
-        m1b = m1c;
-        m1c = m1d;
-        m2b = m2c;
+        q.pf = pf(t < ntiles ? bd : make_int4(0, 0, 0, 0));
+        return q;
+    };
+    // prologue: T_0 .. T_{NS-2} staged, metadata of T_{NS-1} complete and
+    // m1 of T_NS loaded
+    Q qs[NS - 1];
+#pragma unroll
+    for (int i = 0; i < NS - 1; ++i) {
+        const int t = t0 + i * nw;
+        const int m1 = meta1(t);
+        qs[i] = issue(t, mk(m1, meta2(t, m1)), i);
     }
+    int m1a = meta1(t0 + (NS - 1) * nw);
+    int m2a = meta2(t0 + (NS - 1) * nw, m1a);
+    int m1b = meta1(t0 + NS * nw);
+    int it = 0;
+    for (int t = t0; t < ntiles; t += nw, ++it) {
+        const int slot = it % NS;
+        const int tn = t + (NS - 1) * nw;          // tile to stage now
+        const int m1c = meta1(tn + 2 * nw);        // consumed two iterations later
+        const int m2b = meta2(tn + nw, m1b);       // consumed next iteration
+        const Q qn = issue(tn, mk(m1a, m2a), (it + NS - 1) % NS);
+        const Q qc = qs[0];
+#pragma unroll
+        for (int i = 0; i + 1 < NS - 1; ++i) qs[i] = qs[i + 1];
+        qs[NS - 2] = qn;
+        if (!qc.st && lane == 0) mbar_arrive(&bar[slot]);  // keep the phase in step
+        mbar_wait(&bar[slot], (it / NS) & 1);
+        __syncwarp();
+        if (qc.st) {
+            int* i0 = slot_i0(slot);
+            staged(qc.bd, qc.ka, slot_v(slot), i0, i0 + CAP, qc.pf);
+        } else {
+            wide(qc.bd);
+        }
+        __syncwarp();
+        m1a = m1b;
+        m2a = m2b;
+        m1b = m1c;
+    }
+    // tiles staged past the end never arrive: nothing to drain (the
+    // issue() calls beyond ntiles staged nothing)
 }
 
 template <typename T, class Epi, int G>
-__global__ void __launch_bounds__(StreamCfg<T>::kThreads, 2)
+__global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
     csr_stream_kernel(CsrView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
 {
-    using Cfg = StreamCfg<T>;
+    using Cfg = StreamCfg<T, 1>;
     constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bars[Cfg::kWarps][2];
+    __shared__ __align__(8) uint64_t bars[Cfg::kWarps][Cfg::kSlots];
     __shared__ double red_sh[32 * NV];
     if (epi.skip()) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -493,7 +529,7 @@ __global__ void __launch_bounds__(StreamCfg<T>::kThreads, 2)
     };
     warp_tile_loop<T, 1>(
         A.ntiles, A.nnz, A.vals, A.cols, nullptr,
-        smem + size_t(warp) * 2 * Cfg::slot_bytes(1), bars[warp],
+        smem + size_t(warp) * Cfg::kSlots * Cfg::slot_bytes, bars[warp],
         [&](int t) { return (t < A.ntiles && lane < 2) ? __ldg(A.tile_rows + t + lane) : 0; },
         [&](int t, int b) { return (t < A.ntiles && lane < 2) ? __ldg(A.row_ptr + b) : 0; },
         [&](int b, int k) {
@@ -551,13 +587,13 @@ __global__ void __launch_bounds__(StreamCfg<T>::kThreads, 2)
 // row_idx is staged with vals/col_idx; a lane finds its row's extent by
 // binary search over the staged row indices.
 template <typename T, class Epi, int G>
-__global__ void __launch_bounds__(StreamCfg<T>::kThreads, 2)
+__global__ void __launch_bounds__((StreamCfg<T, 2>::kThreads), 2)
     coo_stream_kernel(CooView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
 {
-    using Cfg = StreamCfg<T>;
+    using Cfg = StreamCfg<T, 2>;
     constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bars[Cfg::kWarps][2];
+    __shared__ __align__(8) uint64_t bars[Cfg::kWarps][Cfg::kSlots];
     __shared__ double red_sh[32 * NV];
     if (epi.skip()) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -568,7 +604,7 @@ __global__ void __launch_bounds__(StreamCfg<T>::kThreads, 2)
     struct NoPf {};
     warp_tile_loop<T, 2>(
         A.ntiles, A.nnz, A.vals, A.cols, A.rows,
-        smem + size_t(warp) * 2 * Cfg::slot_bytes(2), bars[warp],
+        smem + size_t(warp) * Cfg::kSlots * Cfg::slot_bytes, bars[warp],
         [&](int t) { return (t < A.ntiles && lane < 2) ? __ldg(A.tile_starts + t + lane) : 0; },
         [&](int t, int k) {
             if (t >= A.ntiles || lane >= 2) return 0;

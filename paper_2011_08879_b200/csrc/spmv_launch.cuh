@@ -97,8 +97,8 @@ void set_smem(K kernel, size_t bytes)
 template <typename T, int NIDX, int G, class K, class View, class Epi>
 void stream_launch(lbk_ctx ctx, K kernel, const View& A, const T* x, const Epi& epi, RedWs ws)
 {
-    using Cfg = StreamCfg<T>;
-    constexpr size_t smem = Cfg::smem_bytes(NIDX);
+    using Cfg = StreamCfg<T, NIDX>;
+    constexpr size_t smem = Cfg::smem_bytes;
     static bool attr = (set_smem(kernel, smem), true);
     (void)attr;
     static int bps = blocks_per_sm(kernel, Cfg::kThreads, smem);
