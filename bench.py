@@ -219,12 +219,20 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_s = float(e2e_t.item())
 
+    # ---- every format / config of §8d on this GPU (rank 0 of a replica run)
+    formats = None
+    if not args.no_formats:
+        try:
+            formats = run_formats(ex, lib, A, x, y, args.steps, args.warmup, args.no_cfg3)
+        except Exception as e:
+            formats = {"error": f"{type(e).__name__}: {e}"}
+
     # ---- CG iterations/s (cfg4): fused single-GPU solver at N = 1, the
     # row-partitioned solver over NCCL (halo exchange + allreduce) at N > 1
     cg = None
+    del A, desc
+    torch.cuda.empty_cache()
     if not args.no_cg:
-        del A, desc
-        torch.cuda.empty_cache()
         try:
             cg = run_cg(ex, world, rank, local_rank, args.cg_dist)
         except Exception as e:  # reported in the line, never fatal for the SpMV metric
@@ -257,11 +265,103 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "gpu_launches": K,
         "clocks": clocks,
     }
+    if formats is not None:
+        line["formats"] = formats
     if cg is not None:
         line["cg"] = cg
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample()
     print(json.dumps(line), flush=True)
+
+
+def time_launches(ex, call, steps: int, warmup: int) -> float:
+    """Mean device time of one launch (CUDA event pair per launch, launches
+    back to back on the executor's stream)."""
+    import torch
+    for _ in range(warmup):
+        call()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for a, b in evs:
+        a.record(ex.stream)
+        call()
+        b.record(ex.stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs) / steps * 1e-3
+
+
+def run_formats(ex, lib, A, x, y, steps: int, warmup: int, no_cfg3: bool) -> dict:
+    """SpMV of every format and precision on the §8d configs: GB/s under the
+    reference byte model (harness.cpp:342-354), GFLOP/s = 2 nnz / t."""
+    import ctypes as C
+    import numpy as np
+    import torch
+
+    from paper_2011_08879_b200 import gen, larch as lk
+
+    peak, _ = measured_peak()
+    out = {"peak_gbs": peak, "note": "GB/s = algorithmic bytes / mean launch time"}
+
+    def meas(key, M, xv, yv, nbytes, nnz):
+        fn = {lk.CsrMatrix: "csr", lk.CooMatrix: "coo", lk.EllMatrix: "ell",
+              lk.SellpMatrix: "sellp"}[type(M)]
+        fn = getattr(lib, f"lbk_spmv_{fn}_{'f32' if xv.values.dtype == torch.float32 else 'f64'}")
+        d = M.desc()
+        xp, yp = C.c_void_p(xv.values.data_ptr()), C.c_void_p(yv.values.data_ptr())
+
+        def call():
+            st = fn(ex.ctx, C.byref(d), xp, yp)
+            if st:
+                lk._check(st, ex.ctx)
+        t = time_launches(ex, call, max(steps, 10), max(warmup, 3))
+        out[key] = {"us": round(t * 1e6, 2), "gbs": round(nbytes / t / 1e9, 1),
+                    "gflops": round(2 * nnz / t / 1e9, 1), "frac": round(nbytes / t / 1e9 / peak, 3),
+                    "bytes": int(nbytes)}
+
+    n, nnz = A.nrows, A.nnz()
+    meas("cfg2_csr_f64", A, x, y, 12 * nnz + 4 * (n + 1) + 16 * n, nnz)
+    Co = lk.csr_to_coo(A)
+    meas("cfg2_coo_f64", Co, x, y, 16 * nnz + 16 * n, nnz)
+    del Co
+    E = lk.csr_to_ell(A)
+    meas("cfg2_ell_f64", E, x, y, 12 * E.width * E.stride + 16 * n, nnz)
+    del E
+    S = lk.csr_to_sellp(A, 32)
+    meas("cfg2_sellp32_f64", S, x, y, 12 * S.col_idx.numel() + 8 * S.nslices + 16 * n, nnz)
+    del S
+    A32 = A.astype(torch.float32)
+    x32 = lk.DenseVector(x.values.float(), ex)
+    y32 = lk.make_vector(ex, n, torch.float32)
+    meas("cfg2_csr_f32", A32, x32, y32, 8 * nnz + 4 * (n + 1) + 8 * n, nnz)
+    del A32
+    torch.cuda.empty_cache()
+    A1 = gen.stencil(ex, "5pt", 1024)
+    x1 = lk.vector_from(ex, gen.seeded_values(A1.ncols, 11))
+    y1 = lk.make_vector(ex, A1.nrows)
+    n1, z1 = A1.nrows, A1.nnz()
+    meas("cfg1_csr_f64", A1, x1, y1, 12 * z1 + 4 * (n1 + 1) + 16 * n1, z1)
+    del A1
+    if not no_cfg3:
+        nn = 1 << 24
+        rp, ci, va = gen.powerlaw_host(nn)
+        A3 = lk.csr_from_host(ex, nn, nn, rp, ci, va)
+        del rp, ci, va
+        z3 = A3.nnz()
+        x3 = lk.vector_from(ex, gen.seeded_values(nn, 11))
+        y3 = lk.make_vector(ex, nn)
+        meas("cfg3_csr_f64", A3, x3, y3, 12 * z3 + 4 * (nn + 1) + 16 * nn, z3)
+        C3 = lk.csr_to_coo(A3)
+        meas("cfg3_coo_f64", C3, x3, y3, 16 * z3 + 16 * nn, z3)
+        del C3
+        A3f = A3.astype(torch.float32)
+        del A3
+        x3f = lk.DenseVector(x3.values.float(), ex)
+        y3f = lk.make_vector(ex, nn, torch.float32)
+        meas("cfg3_csr_f32", A3f, x3f, y3f, 8 * z3 + 4 * (nn + 1) + 8 * nn, z3)
+        del A3f
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_cg(ex, world: int, rank: int, local_rank: int, force_dist: bool = False) -> dict:
@@ -295,6 +395,21 @@ def run_cg(ex, world: int, rank: int, local_rank: int, force_dist: bool = False)
             cg[mode] = {"iterations": r.iterations, "final_rel_residual": r.final_rel_residual,
                         "seconds": r.elapsed, "iters_per_s": r.iterations / r.elapsed,
                         "gflops_ref_model": r.flop_count / r.elapsed / 1e9}
+        del A4, ones, b, xs
+        torch.cuda.empty_cache()
+        # cfg5: BiCGSTAB, 7-pt upwind gamma 0.5, b = A x*, x* = seeded_values(n, 11)
+        A5 = gen.stencil(ex, "7pt", 256, 0.5)
+        xstar = lk.vector_from(ex, gen.seeded_values(A5.ncols, 11))
+        b5 = lk.make_vector(ex, n)
+        lk.spmv(A5, xstar, b5)
+        xs = lk.zeros(ex, n)
+        r = lk.solve(A5, b5, xs, lk.SolverConfig(kind="bicgstab", rel_tol=1e-8, max_iters=20000))
+        cg["bicgstab_cfg5"] = {"config": "cfg5: 7-pt upwind gamma 0.5 256^3, b = A x*, tol 1e-8",
+                               "golden_iterations": "495 (reference) / 498 (parallel)",
+                               "iterations": r.iterations,
+                               "final_rel_residual": r.final_rel_residual, "seconds": r.elapsed,
+                               "iters_per_s": r.iterations / r.elapsed,
+                               "gflops_ref_model": r.flop_count / r.elapsed / 1e9}
         return cg
     # distributed: this rank's rows of the same matrix
     lo, hi = D.part_range(n, world, rank)
@@ -394,6 +509,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cg", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-formats", action="store_true")
+    ap.add_argument("--no-cfg3", action="store_true")
     ap.add_argument("--cg-dist", action="store_true",
                     help="use the row-partitioned solver for the CG leg even at N = 1")
     args = ap.parse_args()
