@@ -221,7 +221,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
 
     # ---- every format / config of §8d on this GPU (rank 0 of a replica run)
     formats = None
-    if not args.no_formats:
+    if not args.no_formats and rank == 0:
         try:
             formats = run_formats(ex, lib, A, x, y, args.steps, args.warmup, args.no_cfg3)
         except Exception as e:
@@ -319,8 +319,62 @@ def run_formats(ex, lib, A, x, y, steps: int, warmup: int, no_cfg3: bool) -> dic
                     "gflops": round(2 * nnz / t / 1e9, 1), "frac": round(nbytes / t / 1e9 / peak, 3),
                     "bytes": int(nbytes)}
 
+    # in-run bandwidth calibration (BabelStream copy / triad, 2 x 1 GiB + 1 GiB)
+    ns = 1 << 27
+    sa = torch.empty(ns, dtype=torch.float64, device=ex.device).fill_(1.0)
+    sb = torch.empty_like(sa).fill_(2.0)
+    sc = torch.empty_like(sa)
+    pa, pb, pc = (C.c_void_p(t.data_ptr()) for t in (sa, sb, sc))
+    t = time_launches(ex, lambda: lk._check(lib.lbk_stream_copy_f64(ex.ctx, ns, pa, pc), ex.ctx),
+                      20, 3)
+    out["stream_copy_gbs"] = round(16 * ns / t / 1e9, 1)
+    t = time_launches(ex, lambda: lk._check(lib.lbk_stream_triad_f64(ex.ctx, ns, 0.4, pb, pc, pa),
+                                            ex.ctx), 20, 3)
+    out["stream_triad_gbs"] = round(24 * ns / t / 1e9, 1)
+    del sa, sb, sc
+    torch.cuda.empty_cache()
+
     n, nnz = A.nrows, A.nnz()
     meas("cfg2_csr_f64", A, x, y, 12 * nnz + 4 * (n + 1) + 16 * n, nnz)
+
+    # device-side assembly and conversions (§8f.1; the reference does these
+    # on the host: 12.2 s for cfg2)
+    def wall(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ex.stream)
+        for _ in range(reps):
+            fn()
+        e1.record(ex.stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+    Co = lk.csr_to_coo(A)
+    perm = torch.randperm(nnz, device=ex.device)
+    rows_s, cols_s, vals_s = Co.row_idx[perm].contiguous(), Co.col_idx[perm].contiguous(), \
+        Co.vals[perm].contiguous()
+    del perm
+    ro = torch.empty_like(rows_s)
+    co = torch.empty_like(cols_s)
+    vo = torch.empty_like(vals_s)
+    nz = C.c_int64()
+
+    def assemble():
+        lk._check(lib.lbk_coo_assemble_f64(ex.ctx, n, n, nnz, C.c_void_p(rows_s.data_ptr()),
+                                           C.c_void_p(cols_s.data_ptr()), C.c_void_p(vals_s.data_ptr()),
+                                           C.c_void_p(ro.data_ptr()), C.c_void_p(co.data_ptr()),
+                                           C.c_void_p(vo.data_ptr()), C.byref(nz)), ex.ctx)
+    conv = {"coo_from_entries_shuffled_ms": round(wall(assemble), 2)}
+    assert nz.value == nnz and torch.equal(ro, Co.row_idx) and torch.equal(co, Co.col_idx)
+    del rows_s, cols_s, vals_s, ro, co, vo
+    conv["coo_to_csr_ms"] = round(wall(lambda: lk.coo_to_csr(Co)), 3)
+    conv["csr_to_coo_ms"] = round(wall(lambda: lk.csr_to_coo(A)), 3)
+    conv["csr_to_ell_ms"] = round(wall(lambda: lk.csr_to_ell(A)), 3)
+    conv["csr_to_sellp32_ms"] = round(wall(lambda: lk.csr_to_sellp(A, 32)), 3)
+    conv["note"] = ("cfg2 (55.7M entries), device; coo_from_entries = bounds check + stable "
+                    "(row, col) sort + duplicate sum (formats.cpp:78-116); output checked equal")
+    out["conversions_cfg2"] = conv
+    torch.cuda.empty_cache()
     Co = lk.csr_to_coo(A)
     meas("cfg2_coo_f64", Co, x, y, 16 * nnz + 16 * n, nnz)
     del Co

@@ -180,6 +180,13 @@ lbk_status lbk_nrm2_f64(lbk_ctx, int64_t n, const double* x, double* result);
 /* result to DEVICE memory (stream-ordered, no sync) */
 lbk_status lbk_dot_f64_dev(lbk_ctx, int64_t n, const double* x, const double* y, double* result_dev);
 
+/* Bandwidth calibration (the reference's stream kernels, reference.cpp:92-130,
+ * and measure_peak_bandwidth, harness.cpp:125-141): c <- a (16 n bytes),
+ * a <- b + s c (24 n bytes).  n even, arrays 16-B aligned. */
+lbk_status lbk_stream_copy_f64(lbk_ctx, int64_t n, const double* a, double* c);
+lbk_status lbk_stream_triad_f64(lbk_ctx, int64_t n, double scalar, const double* b,
+                                const double* c, double* a);
+
 /* ------------------------------------------------------- conversions */
 /* coo_to_csr (formats.cpp:132-155): row histogram + scan; col/vals are
  * identical to the COO arrays (CSR inherits COO order), so only row_ptr is

@@ -84,6 +84,29 @@ void check_n(long long n, const char* what)
     need(n >= 0, LBK_SHAPE_ERROR, std::string(what) + ": negative length");
 }
 
+// BabelStream-style calibration (the reference's measure_peak_bandwidth,
+// src/bench/harness.cpp:125-141, and its stream kernels, reference.cpp:92-130):
+// 128-bit streaming loads/stores, grid = a whole number of waves.
+__global__ void __launch_bounds__(256) stream_copy_kernel(long long n2, const double2* __restrict__ a,
+                                                          double2* __restrict__ c)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
+         i += (long long)gridDim.x * blockDim.x)
+        __stcs(c + i, __ldcs(a + i));
+}
+
+__global__ void __launch_bounds__(256) stream_triad_kernel(long long n2, double s,
+                                                           const double2* __restrict__ b,
+                                                           const double2* __restrict__ c,
+                                                           double2* __restrict__ a)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double2 x = __ldcs(b + i), y = __ldcs(c + i);
+        __stcs(a + i, make_double2(add_rn(x.x, mul_rn(s, y.x)), add_rn(x.y, mul_rn(s, y.y))));
+    }
+}
+
 }  // namespace
 }  // namespace lbk
 
@@ -148,6 +171,36 @@ lbk_status lbk_nrm2_f64(lbk_ctx ctx, int64_t n, const double* x, double* result)
     return guard(ctx, [&] {
         check_n(n, "nrm2");
         *result = n == 0 ? 0.0 : dot_to_host(ctx, n, x, x, true);
+    });
+}
+
+lbk_status lbk_stream_copy_f64(lbk_ctx ctx, int64_t n, const double* a, double* c)
+{
+    if (!ctx) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        check_n(n, "stream_copy");
+        need(n % 2 == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0 &&
+                 (reinterpret_cast<uintptr_t>(c) & 15) == 0,
+             LBK_USAGE_ERROR, "stream_copy: even n and 16-B aligned arrays");
+        if (n == 0) return;
+        stream_copy_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+            n / 2, reinterpret_cast<const double2*>(a), reinterpret_cast<double2*>(c));
+        LBK_LAUNCH_CHECK();
+    });
+}
+
+lbk_status lbk_stream_triad_f64(lbk_ctx ctx, int64_t n, double scalar, const double* b,
+                                const double* c, double* a)
+{
+    if (!ctx) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        check_n(n, "stream_triad");
+        need(n % 2 == 0, LBK_USAGE_ERROR, "stream_triad: even n");
+        if (n == 0) return;
+        stream_triad_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+            n / 2, scalar, reinterpret_cast<const double2*>(b), reinterpret_cast<const double2*>(c),
+            reinterpret_cast<double2*>(a));
+        LBK_LAUNCH_CHECK();
     });
 }
 

@@ -2,6 +2,8 @@
 // bit-exact with the App. B restatement in oracle/port.cpp), the two
 // communicator back ends, device setup and the overlapped SpMV entry point.
 // See dist.cuh for the layout.
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <barrier>
 #include <cstring>
@@ -23,11 +25,53 @@ void part_range(int n, int P, int rank, int* b, int* e)
     *e = static_cast<int>(hi);
 }
 
+// NCCL is resolved at run time (dlopen), not linked: inside a PyTorch
+// process the already-loaded libnccl.so.2 (torch's bundled build) is reused,
+// so the library never drags a second, older NCCL into the process; a pure
+// C/C++ caller gets the system one.  Only the stable core API is used.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclSend) Send = nullptr;
+    decltype(&ncclRecv) Recv = nullptr;
+    decltype(&ncclGroupStart) GroupStart = nullptr;
+    decltype(&ncclGroupEnd) GroupEnd = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+
+const NcclApi& nccl()
+{
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+        a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+        a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+        a.Send = reinterpret_cast<decltype(a.Send)>(dlsym(h, "ncclSend"));
+        a.Recv = reinterpret_cast<decltype(a.Recv)>(dlsym(h, "ncclRecv"));
+        a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
+        a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+        a.GetErrorString =
+            reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        return a;
+    }();
+    need(api.GetUniqueId && api.CommInitRank && api.AllReduce && api.Send && api.Recv &&
+             api.GroupStart && api.GroupEnd && api.GetErrorString && api.CommDestroy,
+         LBK_NCCL_ERROR, "NCCL (libnccl.so.2) could not be loaded");
+    return api;
+}
+
 #define LBK_NCCL(call)                                                                     \
     do {                                                                                   \
         ncclResult_t r_ = (call);                                                          \
         if (r_ != ncclSuccess)                                                             \
-            ::lbk::fail(LBK_NCCL_ERROR, std::string(#call ": ") + ncclGetErrorString(r_)); \
+            ::lbk::fail(LBK_NCCL_ERROR,                                                    \
+                        std::string(#call ": ") + ::lbk::nccl().GetErrorString(r_));       \
     } while (0)
 
 // ------------------------------------------------------------ NCCL
@@ -38,23 +82,24 @@ struct NcclComm final : Comm {
     ncclComm_t comm = nullptr;
     ~NcclComm() override
     {
-        if (comm) ncclCommDestroy(comm);
+        if (comm) nccl().CommDestroy(comm);
     }
     void allreduce_sum(double* dev, int count, cudaStream_t s) override
     {
-        LBK_NCCL(ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, comm, s));
+        LBK_NCCL(nccl().AllReduce(dev, dev, count, ncclDouble, ncclSum, comm, s));
     }
     void exchange(const double* send_buf, const std::vector<int>& so, double* recv,
                   const std::vector<int>& ro, cudaStream_t s) override
     {
-        LBK_NCCL(ncclGroupStart());
+        const NcclApi& N = nccl();
+        LBK_NCCL(N.GroupStart());
         for (int q = 0; q < nranks; ++q) {
             if (q == rank) continue;
             const int ns = so[q + 1] - so[q], nr = ro[q + 1] - ro[q];
-            if (ns > 0) LBK_NCCL(ncclSend(send_buf + so[q], ns, ncclDouble, q, comm, s));
-            if (nr > 0) LBK_NCCL(ncclRecv(recv + ro[q], nr, ncclDouble, q, comm, s));
+            if (ns > 0) LBK_NCCL(N.Send(send_buf + so[q], ns, ncclDouble, q, comm, s));
+            if (nr > 0) LBK_NCCL(N.Recv(recv + ro[q], nr, ncclDouble, q, comm, s));
         }
-        LBK_NCCL(ncclGroupEnd());
+        LBK_NCCL(N.GroupEnd());
     }
     bool async() const override { return true; }
 };
@@ -344,7 +389,7 @@ lbk_status lbk_comm_nccl_unique_id(void* id_out)
     if (!id_out) return LBK_USAGE_ERROR;
     return guard(nullptr, [&] {
         ncclUniqueId id;
-        LBK_NCCL(ncclGetUniqueId(&id));
+        LBK_NCCL(nccl().GetUniqueId(&id));
         std::memcpy(id_out, &id, sizeof(id));
     });
 }
@@ -360,7 +405,7 @@ lbk_status lbk_comm_init_nccl(const void* id, int32_t nranks, int32_t rank, int3
         c->rank = rank;
         ncclUniqueId uid;
         std::memcpy(&uid, id, sizeof(uid));
-        LBK_NCCL(ncclCommInitRank(&c->comm, nranks, uid, rank));
+        LBK_NCCL(nccl().CommInitRank(&c->comm, nranks, uid, rank));
         auto h = std::make_unique<lbk_comm_s>();
         h->impl = c.release();
         *out = h.release();
