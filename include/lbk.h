@@ -221,7 +221,7 @@ lbk_status lbk_validate_coo(lbk_ctx, const lbk_coo* A);
 
 /* ----------------------------------------------------------- solvers */
 /* SolverConfig / SolveResult (krylov.hpp:22-44).  kind: 0 = CG, 1 =
- * BiCGSTAB (krylov.hpp:17; CGS/GMRES are out of scope this round).
+ * BiCGSTAB, 2 = CGS (krylov.hpp:17; GMRES is not provided).
  * residual_mode 0 = reference semantics: true residual ||b - A x||/||b||
  * recomputed every iteration (krylov.cpp:77-84, 145, 221); 1 = recurrence
  * residual for the stopping test, with the true residual verified before

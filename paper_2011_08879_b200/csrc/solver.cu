@@ -22,6 +22,8 @@
 //   CG        K1  q = A p            | <p,q>
 //             K2  x += a p, r -= a q  | <r,r>
 //             K3  t = b - A x         | <t,t>   + fused p = beta p + r
+//   CGS       S1  u, p updates (vec) S2 v = A p | <rt,v>   S3 q, w (vec)
+//             S4  t = A w + x, r updates | <rt,r>    S5 true residual
 //   BiCGSTAB  B2  v = A p            | <rt,v>
 //             B3  s = r - a v         | <s,s>
 //             B4  t = A s            | <t,t>, <t,s>
@@ -93,7 +95,8 @@ struct EpiInit {
     double* __restrict__ p;
     double* __restrict__ rt;  // may be null
     SolverState* st;
-    int bicg;
+    int bicg;                 // 1: BiCGSTAB / CGS preamble (iter = 1, rho = <rt,r>)
+    double* __restrict__ u;   // CGS: u = r for iteration 1 (krylov.cpp:259-261), may be null
     struct Pre {
         double b;
     };
@@ -106,6 +109,7 @@ struct EpiInit {
         r[i] = v;
         p[i] = v;
         if (rt) rt[i] = v;
+        if (u) u[i] = v;
         acc[0] = add_rn(acc[0], mul_rn(v, v));
     }
     __device__ void finish(const double* tot) const
@@ -390,6 +394,120 @@ struct EpiBiB6 {
     }
 };
 
+// CGS (krylov.cpp:233-297), reference semantics (true residual each
+// iteration).  Per iteration: S1 u/p update (vec), S2 v = A p + <rt,v>,
+// S3 q, w (vec), S4 t = A w fused with x += a w, r -= a t and <rt,r> (the
+// next iteration's rho), S5 true residual.
+struct EpiCgsV {
+    static constexpr int NV = 1;
+    double* __restrict__ v;
+    const double* __restrict__ rt;
+    SolverState* st;
+    struct Pre {
+        double rt;
+    };
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ Pre pre(int i) const { return {rt[i]}; }
+    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
+    {
+        v[i] = s;
+        acc[0] = add_rn(acc[0], mul_rn(pr.rt, s));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        st->flops += 2 * st->nnz + 2 * st->n;  // apply + dot(rt, v)
+        const double sigma = tot[0];
+        if (bd(sigma)) {
+            raise_breakdown(st, 3, st->iter);
+            return;
+        }
+        st->alpha = st->rho / sigma;
+    }
+};
+
+struct EpiCgsT {
+    static constexpr int NV = 1;
+    double* __restrict__ t;
+    double* __restrict__ x;
+    double* __restrict__ r;
+    const double* __restrict__ w;
+    const double* __restrict__ rt;
+    SolverState* st;
+    struct Pre {
+        double x, r, w, rt;
+    };
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ Pre pre(int i) const { return {x[i], r[i], w[i], rt[i]}; }
+    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
+    {
+        const double a = st->alpha;
+        t[i] = s;
+        x[i] = add_rn(pr.x, mul_rn(a, pr.w));
+        const double rn = add_rn(pr.r, mul_rn(-a, s));
+        r[i] = rn;
+        acc[0] = add_rn(acc[0], mul_rn(pr.rt, rn));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        // q axpy, w axpy, apply(w), x axpy, r axpy
+        st->flops += 2 * st->n + 2 * st->n + 2 * st->nnz + 2 * st->n + 2 * st->n;
+        st->rho_next = tot[0];  // dot(rt, r) at the top of the next iteration
+    }
+};
+
+struct EpiCgsRes {
+    static constexpr int NV = 1;
+    const double* __restrict__ b;
+    SolverState* st;
+    struct Pre {
+        double b;
+    };
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ Pre pre(int i) const { return {b[i]}; }
+    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int, double s, const Pre& pr, double* acc) const
+    {
+        const double t = add_rn(pr.b, -s);
+        acc[0] = add_rn(acc[0], mul_rn(t, t));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        const long long n = st->n;
+        st->flops += 2 * st->nnz + n + 2 * n + 2 * n;  // true_residual
+        const double rel = sqrt(tot[0]) / st->norm_b;
+        push_hist(st, rel);
+        if (!st->fixed && rel <= st->tol) {
+            st->status = ST_CONVERGED;
+            st->done = 1;
+            return;
+        }
+        if (st->fixed && rel <= kMachineFloor) {
+            st->status = ST_FROZEN;
+            st->done = 1;
+            return;
+        }
+        if (st->iter >= st->limit) {
+            st->status = ST_LIMIT;
+            st->done = 1;
+            return;
+        }
+        // top of iteration iter+1 (krylov.cpp:257-275): rho_next = dot(rt,
+        // r) (reduced in S4), check rho, beta, the u/p updates (9 n flops)
+        const int next = st->iter + 1;
+        st->iter = next;
+        st->flops += 2 * n;
+        if (bd(st->rho)) {
+            raise_breakdown(st, 1, next);
+            return;
+        }
+        st->beta = st->rho_next / st->rho;
+        st->flops += n + 2 * n + n + 2 * n + n + 2 * n;
+        st->rho = st->rho_next;
+    }
+};
+
 // ------------------------------------------------ element-wise steps
 template <class Op>
 __global__ void __launch_bounds__(256) vec_kernel(long long n, Op op, RedWs ws)
@@ -523,6 +641,53 @@ struct OpBiB5 {
         // beta for the p update fused into B6 (checked there)
         st->beta = (tot[0] / st->rho) * (st->alpha / st->omega);
     }
+};
+
+// CGS S1: u = beta q + r; p = beta (beta p + q) + u (krylov.cpp:264-271,
+// the reference's scal/axpy sequence, each step rounded); a no-op in
+// iteration 1, where EpiInit already set u = p = r.
+struct OpCgsUP {
+    static constexpr int NV = 1;
+    double* __restrict__ u;
+    double* __restrict__ p;
+    const double* __restrict__ q;
+    const double* __restrict__ r;
+    SolverState* st;
+    double beta;
+    __device__ bool skip() const
+    {
+        return *(volatile int*)&st->done != 0 || *(volatile int*)&st->iter <= 1;
+    }
+    __device__ void prologue() { beta = st->beta; }
+    __device__ void elem(long long i, double*) const
+    {
+        const double qi = q[i];
+        const double ui = add_rn(mul_rn(qi, beta), r[i]);
+        u[i] = ui;
+        p[i] = add_rn(mul_rn(add_rn(mul_rn(p[i], beta), qi), beta), ui);
+    }
+    __device__ void finish(const double*) const {}
+};
+
+// CGS S3: q = u - alpha v; w = u + q
+struct OpCgsQW {
+    static constexpr int NV = 1;
+    double* __restrict__ q;
+    double* __restrict__ w;
+    const double* __restrict__ u;
+    const double* __restrict__ v;
+    SolverState* st;
+    double alpha;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prologue() { alpha = st->alpha; }
+    __device__ void elem(long long i, double*) const
+    {
+        const double ui = u[i];
+        const double qi = add_rn(ui, mul_rn(-alpha, v[i]));
+        q[i] = qi;
+        w[i] = add_rn(ui, qi);
+    }
+    __device__ void finish(const double*) const {}
 };
 
 // -------------------------------------------------------- operators
@@ -697,8 +862,8 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
     need(cfg != nullptr && res != nullptr, LBK_USAGE_ERROR, "solve: null config/result");
     need(cfg->max_iters >= 1, LBK_CONFIGURATION_ERROR, "max_iters must be positive");
     need(cfg->rel_tol > 0.0, LBK_CONFIGURATION_ERROR, "rel_tol must be positive");
-    need(cfg->kind == 0 || cfg->kind == 1, LBK_CONFIGURATION_ERROR,
-         "solver kind must be 0 (cg) or 1 (bicgstab)");
+    need(cfg->kind >= 0 && cfg->kind <= 2, LBK_CONFIGURATION_ERROR,
+         "solver kind must be 0 (cg), 1 (bicgstab) or 2 (cgs)");
     need(cfg->residual_mode == 0 || (cfg->residual_mode == 1 && cfg->kind == 0),
          LBK_CONFIGURATION_ERROR, "residual_mode 1 is implemented for CG only");
     need(cfg->residual_mode == 0 || cfg->fixed_iters <= 0, LBK_CONFIGURATION_ERROR,
@@ -708,6 +873,7 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
     const bool fixed = cfg->fixed_iters > 0;
     const int limit = fixed ? cfg->fixed_iters : cfg->max_iters;
     const bool bicg = cfg->kind == 1;
+    const bool cgs = cfg->kind == 2;
     const bool recurrence = cfg->residual_mode == 1;
     const long long n = env.n_local(), ne = env.n_ext();
 
@@ -760,11 +926,13 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
     double* r = bufs.get<double>(n);
     double* p = bufs.get<double>(ne);
     double* q = bufs.get<double>(n);  // CG q / BiCGSTAB v
-    double* rt = bicg ? bufs.get<double>(n) : nullptr;
+    double* rt = (bicg || cgs) ? bufs.get<double>(n) : nullptr;
     double* s = bicg ? bufs.get<double>(ne) : nullptr;
-    double* t = bicg ? bufs.get<double>(n) : nullptr;
+    double* t = (bicg || cgs) ? bufs.get<double>(n) : nullptr;
+    double* u = cgs ? bufs.get<double>(n) : nullptr;
+    double* w = cgs ? bufs.get<double>(ne) : nullptr;
 
-    env.apply(x, EpiInit{b, r, p, rt, st, bicg ? 1 : 0});
+    env.apply(x, EpiInit{b, r, p, rt, st, (bicg || cgs) ? 1 : 0, u});
 
     // chunked launch loop; `done` is polled once per chunk
     int* done_host = reinterpret_cast<int*>(ctx->host_pinned);
@@ -772,7 +940,14 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
     int launched = 0;
     for (;;) {
         for (int c = 0; c < chunk && launched < limit; ++c, ++launched) {
-            if (!bicg) {
+            if (cgs) {
+                // v and t share storage: v is dead once S3 has formed q, w
+                env.vec(OpCgsUP{u, p, q, r, st, 0.0});
+                env.apply(p, EpiCgsV{t, rt, st});
+                env.vec(OpCgsQW{q, w, u, t, st, 0.0});
+                env.apply(w, EpiCgsT{t, x, r, w, rt, st});
+                env.apply(x, EpiCgsRes{b, st});
+            } else if (!bicg) {
                 env.apply(p, EpiCgK1{q, p, st});
                 env.vec(OpCgK2{x, r, p, q, st, recurrence ? 1 : 0, 0.0});
                 if (!recurrence) {

@@ -587,7 +587,7 @@ def apply_operator(matrix, v: DenseVector) -> DenseVector:
 
 
 # ----------------------------------------------------------------- solvers
-SOLVER_KINDS = {"cg": 0, "bicgstab": 1}
+SOLVER_KINDS = {"cg": 0, "bicgstab": 1, "cgs": 2}
 
 
 @dataclass

@@ -194,3 +194,34 @@ def test_cfg5_bicgstab_256(ex, lk):
     assert abs(r.iterations - 495) <= 3, r.iterations
     assert r.final_rel_residual <= 1e-8
     assert abs(r.residual_history[1] - 1.136784e-01) <= 1e-6
+
+
+@pytest.mark.parametrize("m,gamma", [(16, 0.0), (24, 0.5)])
+def test_cgs_vs_reference(R, ex, lk, m, gamma):
+    """CGS (krylov.cpp:233-297, §8f.2): iterations within the reference's
+    own executor spread, flop accounting equal, early history agreement."""
+    O = R
+    Rm = O.stencil("7pt", m, gamma)
+    b = O.spmv_csr(Rm, O.seeded_values(Rm.nrows, 11))
+    rr = O.ref_solve(Rm, b, "cgs", rel_tol=1e-8, max_iters=20000)
+    rp = O.ref_solve(Rm, b, "cgs", rel_tol=1e-8, max_iters=20000, exec_kind=1, workers=8)
+    r, x = solve(lk, ex, up(lk, ex, Rm), b, kind="cgs", rel_tol=1e-8, max_iters=20000)
+    spread = max(1, abs(rp.iterations - rr.iterations))
+    assert abs(r.iterations - rr.iterations) <= spread, (r.iterations, rr.iterations)
+    if r.iterations == rr.iterations:
+        assert r.flop_count == rr.flop_count
+    h = np.array(r.residual_history)
+    k = min(10, len(h), len(rr.history))
+    assert np.max(np.abs(h[:k] - rr.history[:k]) / rr.history[:k]) <= 1e-6
+    assert r.converged and r.final_rel_residual <= 1e-8
+    assert relerr(x, rr.x) <= 1e-6
+
+
+def test_cgs_fixed_iters(R, ex, lk):
+    O = R
+    Rm = O.stencil("7pt", 10)
+    b = O.spmv_csr(Rm, np.ones(Rm.nrows))
+    rr = O.ref_solve(Rm, b, "cgs", rel_tol=1e-8, fixed_iters=120)
+    r, _ = solve(lk, ex, up(lk, ex, Rm), b, kind="cgs", rel_tol=1e-8, fixed_iters=120)
+    assert r.iterations == rr.iterations == 120
+    assert len(r.residual_history) == 121
