@@ -221,7 +221,7 @@ lbk_status lbk_validate_coo(lbk_ctx, const lbk_coo* A);
 
 /* ----------------------------------------------------------- solvers */
 /* SolverConfig / SolveResult (krylov.hpp:22-44).  kind: 0 = CG, 1 =
- * BiCGSTAB, 2 = CGS (krylov.hpp:17; GMRES is not provided).
+ * BiCGSTAB, 2 = CGS, 3 = restarted GMRES (krylov.hpp:17).
  * residual_mode 0 = reference semantics: true residual ||b - A x||/||b||
  * recomputed every iteration (krylov.cpp:77-84, 145, 221); 1 = recurrence
  * residual for the stopping test, with the true residual verified before
@@ -232,6 +232,7 @@ typedef struct lbk_solver_cfg {
     double rel_tol;        /* default 1e-10 */
     int32_t fixed_iters;   /* <= 0: unset */
     int32_t residual_mode; /* 0 true residual each iteration, 1 recurrence */
+    int32_t gmres_restart; /* kind 3: Krylov basis per cycle, [1, max_iters] (krylov.hpp:28) */
 } lbk_solver_cfg;
 
 typedef struct lbk_solve_result {

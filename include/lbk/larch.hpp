@@ -9,7 +9,7 @@
 //   arrays      include/larch/core/device_array.hpp:57-171  (DeviceArray)
 //   formats     include/larch/matrix/formats.hpp:20-94      (+ Ell, Sellp)
 //   kernels     include/larch/kernels/kernels.hpp:79-97     (+ alpha/beta)
-//   solvers     include/larch/solver/krylov.hpp:17-60       (cg, bicgstab, cgs)
+//   solvers     include/larch/solver/krylov.hpp:17-60       (cg, bicgstab, cgs, gmres)
 //
 // Same names, argument meaning and error behaviour, so code written
 // against the reference recompiles against this header with
@@ -574,9 +574,6 @@ namespace detail {
 template <class M, class F>
 SolveResult solve_with(const M& A, const DenseVector& b, DenseVector& x, const SolverConfig& c, F&& call)
 {
-    if (c.kind == SolverKind::gmres)
-        throw ConfigurationError(std::string("solver kind ") + to_string(c.kind) +
-                                 " is not provided by the B200 backend");
     if (c.fixed_iters && *c.fixed_iters < 1) throw ConfigurationError("fixed_iters must be positive");
     if (A.nrows != A.ncols)
         throw ShapeError("solve requires a square matrix, got " + std::to_string(A.nrows) + "x" +
@@ -585,10 +582,9 @@ SolveResult solve_with(const M& A, const DenseVector& b, DenseVector& x, const S
     same_size(x.size(), static_cast<std::size_t>(A.nrows), "solve");
     same_space(A.executor(), b.executor(), "solve");
     same_space(A.executor(), x.executor(), "solve");
-    lbk_solver_cfg cfg{c.kind == SolverKind::cg ? 0 : (c.kind == SolverKind::bicgstab ? 1 : 2),
-                       c.max_iters, c.rel_tol,
+    lbk_solver_cfg cfg{static_cast<int32_t>(c.kind), c.max_iters, c.rel_tol,
                        c.fixed_iters ? *c.fixed_iters : 0,
-                       c.residual_mode == ResidualMode::recurrence ? 1 : 0};
+                       c.residual_mode == ResidualMode::recurrence ? 1 : 0, c.gmres_restart};
     lbk_solve_result r{};
     std::vector<double> hist(static_cast<std::size_t>(c.fixed_iters ? *c.fixed_iters : c.max_iters) + 2);
     auto e = A.executor();

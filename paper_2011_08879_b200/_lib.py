@@ -66,7 +66,8 @@ class lbk_dist_map_info_t(C.Structure):
 
 class lbk_solver_cfg(C.Structure):
     _fields_ = [("kind", C.c_int32), ("max_iters", C.c_int32), ("rel_tol", C.c_double),
-                ("fixed_iters", C.c_int32), ("residual_mode", C.c_int32)]
+                ("fixed_iters", C.c_int32), ("residual_mode", C.c_int32),
+                ("gmres_restart", C.c_int32)]
 
 
 class lbk_solve_result(C.Structure):

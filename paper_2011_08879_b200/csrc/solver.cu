@@ -45,6 +45,7 @@ namespace {
 
 constexpr double kBreakdownEps = 1e-30;  // krylov.cpp:18
 constexpr double kMachineFloor = 1e-13;  // krylov.cpp:23
+constexpr double kHappyEps = 1e-14;      // krylov.cpp:24
 
 enum : int { ST_RUNNING = 0, ST_CONVERGED = 1, ST_LIMIT = 2, ST_BREAKDOWN = 3, ST_FROZEN = 4 };
 
@@ -66,6 +67,23 @@ struct SolverState {
     long long n, nnz;
     long long flops;
     double* hist;
+    struct GmresState* gm;  // GMRES only
+};
+
+// Restarted GMRES (krylov.cpp:308-443): the Hessenberg column, Givens
+// rotations, rotated rhs and back-substitution are O(restart^2) scalars that
+// the reference keeps on the host; here they live in device memory and are
+// advanced by the finisher threads, so no host round trip per step.
+struct GmresState {
+    int restart;
+    int steps;        // steps done in this cycle
+    int cycle_done;
+    int happy;
+    int cycle_limit;  // min(restart, limit - iterations)
+    int iterations;   // completed steps over all cycles
+    double beta, hnext;
+    double* H;        // (restart + 1) x restart, row-major [i * restart + j]
+    double *gc, *gs, *g, *y;
 };
 
 __device__ __forceinline__ bool bd(double v) { return fabs(v) < kBreakdownEps; }
@@ -508,6 +526,118 @@ struct EpiCgsRes {
     }
 };
 
+// ----------------------------------------------------------- GMRES
+__device__ bool gm_step_skip(const SolverState* st, int jj)
+{
+    const GmresState* G = st->gm;
+    return *(volatile const int*)&st->done != 0 || *(volatile const int*)&G->cycle_done != 0 ||
+           jj >= *(volatile const int*)&G->cycle_limit;
+}
+
+// r = b - A x into V0 and <r,r>: the initial true residual (first = 1,
+// krylov.cpp:420-424) or the end-of-cycle true residual (krylov.cpp:397-399);
+// either way it is also the next cycle's initial residual (same x, same
+// bits), whose flops are counted when that cycle starts.
+struct EpiGmRes {
+    static constexpr int NV = 1;
+    const double* __restrict__ b;
+    double* __restrict__ v0;
+    SolverState* st;
+    int first;
+    struct Pre {
+        double b;
+    };
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ Pre pre(int i) const { return {b[i]}; }
+    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
+    {
+        const double t = add_rn(pr.b, -s);
+        v0[i] = t;
+        acc[0] = add_rn(acc[0], mul_rn(t, t));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        GmresState* G = st->gm;
+        const long long n = st->n, nnz = st->nnz;
+        const double rr = tot[0];
+        const double rel = sqrt(rr) / st->norm_b;
+        st->flops += 2 * nnz + n + 2 * n + 2 * n;  // true_residual
+        if (first) {
+            st->hist_len = 0;
+            push_hist(st, rel);
+            if (!st->fixed && rel <= st->tol) {
+                st->status = ST_CONVERGED;
+                st->done = 1;
+                return;
+            }
+        } else {
+            G->iterations += G->steps;
+            st->hist[st->hist_len - 1] = rel;  // replaces the last estimate
+            st->last_rel = rel;
+            if (!st->fixed && rel <= st->tol) {
+                st->status = ST_CONVERGED;
+                st->done = 1;
+                return;
+            }
+            if (st->fixed && rel <= kMachineFloor) {
+                st->status = ST_FROZEN;
+                st->done = 1;
+                return;
+            }
+            if (G->iterations >= st->limit) {
+                st->status = ST_LIMIT;
+                st->done = 1;
+                return;
+            }
+        }
+        // next cycle: initial_residual + norm (krylov.cpp:315-316)
+        st->flops += 2 * nnz + n + 2 * n + 2 * n;
+        const double beta = sqrt(rr);
+        G->steps = 0;
+        G->happy = 0;
+        if (beta == 0.0) {
+            // zero residual: nothing to iterate on (krylov.cpp:426-433)
+            G->cycle_done = 1;
+            st->status = st->fixed ? ST_FROZEN : ST_CONVERGED;
+            st->done = 1;
+            return;
+        }
+        st->flops += n;  // scal(1 / beta)
+        G->beta = beta;
+        G->g[0] = beta;
+        const int left = st->limit - G->iterations;
+        G->cycle_limit = G->restart < left ? G->restart : left;
+        G->cycle_done = 0;
+    }
+};
+
+// S1 of step jj: w = A v_jj, <v_0, w> (the first MGS dot, krylov.cpp:339-344)
+struct EpiGmApply {
+    static constexpr int NV = 1;
+    double* __restrict__ w;
+    const double* __restrict__ v0;
+    SolverState* st;
+    int jj;
+    struct Pre {
+        double v0;
+    };
+    __device__ bool skip() const { return gm_step_skip(st, jj); }
+    __device__ Pre pre(int i) const { return {v0[i]}; }
+    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
+    {
+        w[i] = s;
+        acc[0] = add_rn(acc[0], mul_rn(pr.v0, s));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        GmresState* G = st->gm;
+        st->flops += 2 * st->nnz + 2 * st->n;
+        G->H[0 * G->restart + jj] = tot[0];
+    }
+};
+
 // ------------------------------------------------ element-wise steps
 template <class Op>
 __global__ void __launch_bounds__(256) vec_kernel(long long n, Op op, RedWs ws)
@@ -690,6 +820,118 @@ struct OpCgsQW {
     __device__ void finish(const double*) const {}
 };
 
+// MGS pass i of step jj (i >= 1): w -= h[i-1][jj] v_{i-1}, then <v_i, w>;
+// i == jj + 1 is the closing pass: w -= h[jj][jj] v_jj, then <w, w> = hnext^2
+// and the Givens update of column jj (krylov.cpp:340-375).
+struct OpGmMgs {
+    static constexpr int NV = 1;
+    double* __restrict__ w;
+    const double* __restrict__ vprev;
+    const double* __restrict__ vi;  // null on the closing pass
+    SolverState* st;
+    int i, jj;
+    double h;
+    __device__ bool skip() const { return gm_step_skip(st, jj); }
+    __device__ void prologue() { h = st->gm->H[(i - 1) * st->gm->restart + jj]; }
+    __device__ void elem(long long k, double* acc) const
+    {
+        const double wn = add_rn(w[k], mul_rn(-h, vprev[k]));
+        w[k] = wn;
+        acc[0] = add_rn(acc[0], mul_rn(vi ? vi[k] : wn, wn));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        GmresState* G = st->gm;
+        const int m = G->restart;
+        double* H = G->H;
+        st->flops += 2 * st->n + 2 * st->n;  // axpy + dot / norm
+        if (vi) {
+            H[i * m + jj] = tot[0];
+            return;
+        }
+        const double hnext = sqrt(tot[0]);
+        G->hnext = hnext;
+        for (int r = 0; r < jj; ++r) {
+            const double a = H[r * m + jj], c = H[(r + 1) * m + jj];
+            const double upper = add_rn(mul_rn(G->gc[r], a), mul_rn(G->gs[r], c));
+            H[(r + 1) * m + jj] = add_rn(mul_rn(-G->gs[r], a), mul_rn(G->gc[r], c));
+            H[r * m + jj] = upper;
+        }
+        const double denom = hypot(H[jj * m + jj], hnext);
+        if (bd(denom)) {
+            raise_breakdown(st, 5, G->steps + 1);
+            return;
+        }
+        G->gc[jj] = H[jj * m + jj] / denom;
+        G->gs[jj] = hnext / denom;
+        H[jj * m + jj] = denom;
+        G->g[jj + 1] = mul_rn(-G->gs[jj], G->g[jj]);
+        G->g[jj] = mul_rn(G->gc[jj], G->g[jj]);
+        G->steps += 1;
+        push_hist(st, fabs(G->g[jj + 1]) / st->norm_b);  // in-cycle estimate
+        G->happy = hnext < kHappyEps;
+        if (G->happy) {
+            G->cycle_done = 1;
+            return;
+        }
+        st->flops += st->n;  // scal(1 / hnext)
+        if ((!st->fixed && st->last_rel <= st->tol) || G->steps >= G->cycle_limit)
+            G->cycle_done = 1;
+    }
+};
+
+// v_{jj+1} = w / hnext (krylov.cpp:369); skipped when the cycle ends here.
+struct OpGmScale {
+    static constexpr int NV = 1;
+    double* __restrict__ v;
+    const double* __restrict__ w;  // null: scale v in place by 1 / beta
+    SolverState* st;
+    int jj;
+    double inv;
+    __device__ bool skip() const { return gm_step_skip(st, jj); }
+    __device__ void prologue() { inv = 1.0 / (w ? st->gm->hnext : st->gm->beta); }
+    __device__ void elem(long long k, double*) const { v[k] = mul_rn(w ? w[k] : v[k], inv); }
+    __device__ void finish(const double*) const {}
+};
+
+// Back substitution of the rotated triangle (krylov.cpp:381-391).
+__global__ void gmres_backsub_kernel(SolverState* st)
+{
+    if (st->done) return;
+    GmresState* G = st->gm;
+    const int m = G->restart, steps = G->steps;
+    for (int i = steps - 1; i >= 0; --i) {
+        double sum = G->g[i];
+        for (int k = i + 1; k < steps; ++k) sum = add_rn(sum, -mul_rn(G->H[i * m + k], G->y[k]));
+        if (bd(G->H[i * m + i])) {
+            raise_breakdown(st, 6, i + 1);
+            return;
+        }
+        G->y[i] = sum / G->H[i * m + i];
+    }
+    st->flops += static_cast<long long>(steps) * steps;
+}
+
+// x += y_0 v_0 + y_1 v_1 + ... in the reference's axpy order (krylov.cpp:392-394)
+struct OpGmUpdate {
+    static constexpr int NV = 1;
+    double* __restrict__ x;
+    const double* __restrict__ V;
+    long long ld;
+    SolverState* st;
+    int steps;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prologue() { steps = st->gm->steps; }
+    __device__ void elem(long long k, double*) const
+    {
+        const double* y = st->gm->y;
+        double v = x[k];
+        for (int i = 0; i < steps; ++i) v = add_rn(v, mul_rn(__ldg(y + i), V[i * ld + k]));
+        x[k] = v;
+    }
+    __device__ void finish(const double*) const { st->flops += 2LL * steps * st->n; }
+};
+
 // -------------------------------------------------------- operators
 struct CsrOp {
     CsrView<double> A;
@@ -747,6 +989,8 @@ const char* breakdown_what(int w)
     case 1: return "division by vanishing rho";
     case 2: return "division by vanishing omega";
     case 3: return "division by vanishing <rt, Ap>";
+    case 5: return "division by vanishing Givens denominator";
+    case 6: return "division by vanishing triangular diagonal";
     default: return "division by vanishing <t, t>";
     }
 }
@@ -854,6 +1098,51 @@ struct DistEnv {
     }
 };
 
+// Result assembly shared by every solver: copy x back, read the state and
+// the history, apply the fixed-iteration freeze padding (krylov.cpp:135-137)
+// and raise BreakdownError with its iteration.
+template <class Env>
+void finish_solve(lbk_ctx ctx, Env& env, SolverState* st, double* hist, double* x, double* x_user,
+                  long long n, int limit, const lbk_solver_cfg* cfg, lbk_solve_result* res,
+                  double* history, int hist_cap, cudaEvent_t ev0, cudaEvent_t ev1)
+{
+    SolverState h{};
+    if (env.ext_x() && n)
+        LBK_CUDA(cudaMemcpyAsync(x_user, x, size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+    LBK_CUDA(cudaEventRecord(ev1, ctx->stream));
+    LBK_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    LBK_CUDA(cudaStreamSynchronize(ctx->stream));
+    float ms = 0;
+    LBK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+
+    std::vector<double> hv(static_cast<size_t>(h.hist_len));
+    if (h.hist_len)
+        LBK_CUDA(cudaMemcpy(hv.data(), hist, hv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    if (h.status == ST_FROZEN) {
+        // krylov.cpp:135-137: frozen iterations repeat the last entry
+        while (static_cast<int>(hv.size()) < limit + 1) hv.push_back(hv.back());
+    }
+    res->iterations = static_cast<int>(hv.size()) - 1;
+    res->history_len = static_cast<int>(hv.size());
+    res->final_rel_residual = hv.back();
+    res->converged = res->final_rel_residual <= cfg->rel_tol ? 1 : 0;
+    res->flop_count = h.flops;
+    res->elapsed = ms * 1e-3;
+    if (history) {
+        const int m = res->history_len < hist_cap ? res->history_len : hist_cap;
+        for (int i = 0; i < m; ++i) history[i] = hv[i];
+    }
+    if (h.status == ST_BREAKDOWN) {
+        res->breakdown_iter = h.breakdown_iter;
+        Error e(LBK_BREAKDOWN, std::string(breakdown_what(h.breakdown_what)) + " at iteration " +
+                                   std::to_string(h.breakdown_iter));
+        throw e;
+    }
+}
+
 template <class Env>
 void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lbk_solver_cfg* cfg,
                 lbk_solve_result* res, double* history, int hist_cap)
@@ -862,8 +1151,10 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
     need(cfg != nullptr && res != nullptr, LBK_USAGE_ERROR, "solve: null config/result");
     need(cfg->max_iters >= 1, LBK_CONFIGURATION_ERROR, "max_iters must be positive");
     need(cfg->rel_tol > 0.0, LBK_CONFIGURATION_ERROR, "rel_tol must be positive");
-    need(cfg->kind >= 0 && cfg->kind <= 2, LBK_CONFIGURATION_ERROR,
-         "solver kind must be 0 (cg), 1 (bicgstab) or 2 (cgs)");
+    need(cfg->kind >= 0 && cfg->kind <= 3, LBK_CONFIGURATION_ERROR,
+         "solver kind must be 0 (cg), 1 (bicgstab), 2 (cgs) or 3 (gmres)");
+    need(cfg->kind != 3 || (cfg->gmres_restart >= 1 && cfg->gmres_restart <= cfg->max_iters),
+         LBK_CONFIGURATION_ERROR, "gmres_restart must lie in [1, max_iters]");
     need(cfg->residual_mode == 0 || (cfg->residual_mode == 1 && cfg->kind == 0),
          LBK_CONFIGURATION_ERROR, "residual_mode 1 is implemented for CG only");
     need(cfg->residual_mode == 0 || cfg->fixed_iters <= 0, LBK_CONFIGURATION_ERROR,
@@ -874,6 +1165,7 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
     const int limit = fixed ? cfg->fixed_iters : cfg->max_iters;
     const bool bicg = cfg->kind == 1;
     const bool cgs = cfg->kind == 2;
+    const bool gmres = cfg->kind == 3;
     const bool recurrence = cfg->residual_mode == 1;
     const long long n = env.n_local(), ne = env.n_ext();
 
@@ -923,6 +1215,46 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
         if (n) LBK_CUDA(cudaMemcpyAsync(x, x_user, size_t(n) * sizeof(double),
                                         cudaMemcpyDeviceToDevice, ctx->stream));
     }
+    if (gmres) {
+        const int m = cfg->gmres_restart;
+        auto* G = bufs.get<GmresState>(1);
+        GmresState gh{};
+        gh.restart = m;
+        gh.H = bufs.get<double>(size_t(m + 1) * m);
+        gh.gc = bufs.get<double>(m);
+        gh.gs = bufs.get<double>(m);
+        gh.g = bufs.get<double>(m + 1);
+        gh.y = bufs.get<double>(m);
+        LBK_CUDA(cudaMemcpyAsync(G, &gh, sizeof(gh), cudaMemcpyHostToDevice, ctx->stream));
+        h.gm = G;
+        LBK_CUDA(cudaMemcpyAsync(st, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+        double* V = bufs.get<double>(size_t(m + 1) * ne);
+        double* w = bufs.get<double>(n);
+        env.apply(x, EpiGmRes{b, V, st, 1});
+        env.vec(OpGmScale{V, nullptr, st, 0, 0.0});
+        int* done_host = reinterpret_cast<int*>(ctx->host_pinned);
+        for (;;) {
+            for (int jj = 0; jj < m; ++jj) {
+                env.apply(V + size_t(jj) * ne, EpiGmApply{w, V, st, jj});
+                for (int i = 1; i <= jj + 1; ++i)
+                    env.vec(OpGmMgs{w, V + size_t(i - 1) * ne, i <= jj ? V + size_t(i) * ne : nullptr,
+                                    st, i, jj, 0.0});
+                env.vec(OpGmScale{V + size_t(jj + 1) * ne, w, st, jj, 0.0});
+            }
+            gmres_backsub_kernel<<<1, 1, 0, ctx->stream>>>(st);
+            LBK_LAUNCH_CHECK();
+            env.vec(OpGmUpdate{x, V, ne, st, 0});
+            env.apply(x, EpiGmRes{b, V, st, 0});
+            env.vec(OpGmScale{V, nullptr, st, 0, 0.0});
+            LBK_CUDA(cudaMemcpyAsync(done_host, &st->done, sizeof(int), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+            LBK_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (*done_host) break;
+        }
+        finish_solve(ctx, env, st, hist, x, x_user, n, limit, cfg, res, history, hist_cap, ev0, ev1);
+        return;
+    }
+
     double* r = bufs.get<double>(n);
     double* p = bufs.get<double>(ne);
     double* q = bufs.get<double>(n);  // CG q / BiCGSTAB v
@@ -969,40 +1301,7 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
         LBK_CUDA(cudaStreamSynchronize(ctx->stream));
         if (*done_host || launched >= limit) break;
     }
-    if (env.ext_x() && n)
-        LBK_CUDA(cudaMemcpyAsync(x_user, x, size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice,
-                                 ctx->stream));
-    LBK_CUDA(cudaEventRecord(ev1, ctx->stream));
-    LBK_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
-    LBK_CUDA(cudaStreamSynchronize(ctx->stream));
-    float ms = 0;
-    LBK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
-
-    std::vector<double> hv(static_cast<size_t>(h.hist_len));
-    if (h.hist_len)
-        LBK_CUDA(cudaMemcpy(hv.data(), hist, hv.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    if (h.status == ST_FROZEN) {
-        // krylov.cpp:135-137: frozen iterations repeat the last entry
-        while (static_cast<int>(hv.size()) < limit + 1) hv.push_back(hv.back());
-    }
-    res->iterations = static_cast<int>(hv.size()) - 1;
-    res->history_len = static_cast<int>(hv.size());
-    res->final_rel_residual = hv.back();
-    res->converged = res->final_rel_residual <= cfg->rel_tol ? 1 : 0;
-    res->flop_count = h.flops;
-    res->elapsed = ms * 1e-3;
-    if (history) {
-        const int m = res->history_len < hist_cap ? res->history_len : hist_cap;
-        for (int i = 0; i < m; ++i) history[i] = hv[i];
-    }
-    if (h.status == ST_BREAKDOWN) {
-        res->breakdown_iter = h.breakdown_iter;
-        Error e(LBK_BREAKDOWN, std::string(breakdown_what(h.breakdown_what)) + " at iteration " +
-                                   std::to_string(h.breakdown_iter));
-        throw e;
-    }
+    finish_solve(ctx, env, st, hist, x, x_user, n, limit, cfg, res, history, hist_cap, ev0, ev1);
 }
 
 }  // namespace

@@ -236,7 +236,8 @@ class DistCsrMatrix:
             raise ConfigurationError(f"solver kind {config.kind!r} not provided by the B200 backend")
         cfg = L.lbk_solver_cfg(SOLVER_KINDS[config.kind], int(config.max_iters),
                                float(config.rel_tol), int(config.fixed_iters or 0),
-                               1 if config.residual_mode == "recurrence" else 0)
+                               1 if config.residual_mode == "recurrence" else 0,
+                               int(config.gmres_restart))
         res = L.lbk_solve_result()
         cap = int(config.fixed_iters or config.max_iters) + 2
         hist = np.empty(cap, np.float64)

@@ -587,7 +587,7 @@ def apply_operator(matrix, v: DenseVector) -> DenseVector:
 
 
 # ----------------------------------------------------------------- solvers
-SOLVER_KINDS = {"cg": 0, "bicgstab": 1, "cgs": 2}
+SOLVER_KINDS = {"cg": 0, "bicgstab": 1, "cgs": 2, "gmres": 3}
 
 
 @dataclass
@@ -628,7 +628,8 @@ def solve(matrix, b: DenseVector, x: DenseVector, config: SolverConfig) -> Solve
     _f64(x, "solve")
     cfg = L.lbk_solver_cfg(SOLVER_KINDS[config.kind], int(config.max_iters), float(config.rel_tol),
                            int(config.fixed_iters or 0),
-                           1 if config.residual_mode == "recurrence" else 0)
+                           1 if config.residual_mode == "recurrence" else 0,
+                           int(config.gmres_restart))
     res = L.lbk_solve_result()
     cap = int(config.fixed_iters or config.max_iters) + 2
     hist = np.empty(cap, np.float64)

@@ -213,6 +213,7 @@ static void test_blas1_and_errors(std::shared_ptr<larch::Executor> e)
     auto s = larch::zeros(e, 2);
     larch::SolverConfig cfg;
     cfg.kind = larch::SolverKind::gmres;
+    cfg.gmres_restart = 0;  // krylov.cpp:466-471: must lie in [1, max_iters]
     HostCsr sq{2, 2, {0, 1, 2}, {0, 1}, {1, 1}};
     auto Sq = upload(e, sq);
     CHECK_THROWS_AS(larch::solve(Sq, s, s, cfg), larch::ConfigurationError);

@@ -108,7 +108,11 @@ def test_config_errors(ex, lk):
     with pytest.raises(lk.ConfigurationError):
         solve(lk, ex, A, np.ones(2), kind="cg", rel_tol=0.0)
     with pytest.raises(lk.ConfigurationError):
-        solve(lk, ex, A, np.ones(2), kind="gmres")
+        solve(lk, ex, A, np.ones(2), kind="gmres", gmres_restart=0)
+    with pytest.raises(lk.ConfigurationError):
+        solve(lk, ex, A, np.ones(2), kind="gmres", max_iters=10, gmres_restart=11)
+    with pytest.raises(lk.ConfigurationError):
+        solve(lk, ex, A, np.ones(2), kind="minres")
     B = lk.csr_from_host(ex, 2, 3, [0, 1, 2], [0, 1], [1.0, 1.0])
     with pytest.raises(lk.ShapeError):
         solve(lk, ex, B, np.ones(2), kind="cg")
@@ -225,3 +229,37 @@ def test_cgs_fixed_iters(R, ex, lk):
     r, _ = solve(lk, ex, up(lk, ex, Rm), b, kind="cgs", rel_tol=1e-8, fixed_iters=120)
     assert r.iterations == rr.iterations == 120
     assert len(r.residual_history) == 121
+
+
+@pytest.mark.parametrize("m,gamma,restart", [(12, 0.0, 30), (16, 0.5, 30), (12, 0.5, 5)])
+def test_gmres_vs_reference(R, ex, lk, m, gamma, restart):
+    """Restarted GMRES (krylov.cpp:308-443, §8f.2): MGS on the device, the
+    Givens / back-substitution scalars advanced by finisher threads."""
+    O = R
+    Rm = O.stencil("7pt", m, gamma)
+    b = O.spmv_csr(Rm, O.seeded_values(Rm.nrows, 11))
+    rr = O.ref_solve(Rm, b, "gmres", rel_tol=1e-8, max_iters=20000, restart=restart)
+    rp = O.ref_solve(Rm, b, "gmres", rel_tol=1e-8, max_iters=20000, restart=restart,
+                     exec_kind=1, workers=8)
+    r, x = solve(lk, ex, up(lk, ex, Rm), b, kind="gmres", rel_tol=1e-8, max_iters=20000,
+                 gmres_restart=restart)
+    spread = max(1, abs(rp.iterations - rr.iterations))
+    assert abs(r.iterations - rr.iterations) <= spread, (r.iterations, rr.iterations)
+    if r.iterations == rr.iterations:
+        assert r.flop_count == rr.flop_count
+    h = np.array(r.residual_history)
+    k = min(10, len(h), len(rr.history))
+    assert np.max(np.abs(h[:k] - rr.history[:k]) / rr.history[:k]) <= 1e-6
+    assert r.converged and r.final_rel_residual <= 1e-8
+    assert relerr(x, rr.x) <= 1e-6
+
+
+def test_gmres_fixed_iters(R, ex, lk):
+    O = R
+    Rm = O.stencil("7pt", 8, 0.5)
+    b = O.spmv_csr(Rm, np.ones(Rm.nrows))
+    rr = O.ref_solve(Rm, b, "gmres", rel_tol=1e-8, fixed_iters=50, restart=7)
+    r, _ = solve(lk, ex, up(lk, ex, Rm), b, kind="gmres", rel_tol=1e-8, fixed_iters=50,
+                 gmres_restart=7)
+    assert r.iterations == rr.iterations == 50
+    assert len(r.residual_history) == 51
