@@ -46,6 +46,7 @@ typedef enum lbk_status {
     LBK_FORMAT_ERROR = 8,          /* FormatError          error.hpp:100 */
     LBK_BREAKDOWN = 9,             /* BreakdownError       error.hpp:115 */
     LBK_BENCHMARK_INTEGRITY = 10,  /* BenchmarkIntegrityError error.hpp:128 */
+    LBK_UNSUPPORTED_FORMAT = 11,   /* UnsupportedFormatError (a FormatError) error.hpp:108 */
     LBK_CUDA_ERROR = 20,           /* device/runtime failure (new) */
     LBK_NCCL_ERROR = 21,           /* collective failure (new) */
     LBK_INTERNAL = 99
@@ -218,6 +219,19 @@ lbk_status lbk_csr_to_sellp(lbk_ctx, const lbk_csr* A, int32_t slice_size,
 /* validate(Csr/Coo) (formats.cpp:182-242): LBK_FORMAT_ERROR on violation. */
 lbk_status lbk_validate_csr(lbk_ctx, const lbk_csr* A);
 lbk_status lbk_validate_coo(lbk_ctx, const lbk_coo* A);
+
+/* MatrixMarket ingestion (read_matrix_market, reference io.hpp:25-28 /
+ * io.cpp:71-191): host parse with the reference's acceptance rules and
+ * messages; the entry list (symmetric files expanded, 0-based) is then
+ * assembled on the device with lbk_coo_assemble_f64.  lbk_mm_read returns
+ * LBK_FORMAT_ERROR / LBK_UNSUPPORTED_FORMAT with lbk_mm_last_error(). */
+typedef struct lbk_mm_s* lbk_mm;
+lbk_status lbk_mm_read(const char* path, lbk_mm* out);
+const char* lbk_mm_last_error(void);
+lbk_status lbk_mm_info(lbk_mm m, int32_t* nrows, int32_t* ncols, int64_t* n_entries);
+/* host pointers owned by the handle, valid until lbk_mm_free */
+lbk_status lbk_mm_entries(lbk_mm m, const int32_t** rows, const int32_t** cols, const double** vals);
+lbk_status lbk_mm_free(lbk_mm m);
 
 /* ----------------------------------------------------------- solvers */
 /* SolverConfig / SolveResult (krylov.hpp:22-44).  kind: 0 = CG, 1 =

@@ -8,6 +8,7 @@
 //   executor    include/larch/core/executor.hpp:130-262     (cuda kind)
 //   arrays      include/larch/core/device_array.hpp:57-171  (DeviceArray)
 //   formats     include/larch/matrix/formats.hpp:20-94      (+ Ell, Sellp)
+//   io          include/larch/matrix/io.hpp:25-28           (read_matrix_market)
 //   kernels     include/larch/kernels/kernels.hpp:79-97     (+ alpha/beta)
 //   solvers     include/larch/solver/krylov.hpp:17-60       (cg, bicgstab, cgs, gmres)
 //
@@ -19,6 +20,7 @@
 #define LBK_LARCH_HPP
 
 #include <cstdint>
+#include <filesystem>
 #include <memory>
 #include <optional>
 #include <span>
@@ -44,6 +46,7 @@ class PlacementError : public Error { using Error::Error; };
 class UsageError : public Error { using Error::Error; };
 class DispatchError : public Error { using Error::Error; };
 class FormatError : public Error { using Error::Error; };
+class UnsupportedFormatError : public FormatError { using FormatError::FormatError; };
 class BenchmarkIntegrityError : public Error { using Error::Error; };
 class DeviceError : public Error { using Error::Error; };  // CUDA/NCCL (new)
 class BreakdownError : public Error {
@@ -66,6 +69,7 @@ inline void check(lbk_status s, lbk_ctx ctx = nullptr, int iter = -1)
     case LBK_CONFIGURATION_ERROR: throw ConfigurationError(m);
     case LBK_OUT_OF_MEMORY: throw OutOfMemoryError(m);
     case LBK_FORMAT_ERROR: throw FormatError(m);
+    case LBK_UNSUPPORTED_FORMAT: throw UnsupportedFormatError(m);
     case LBK_BREAKDOWN: throw BreakdownError(m, iter);
     case LBK_BENCHMARK_INTEGRITY: throw BenchmarkIntegrityError(m);
     case LBK_CUDA_ERROR:
@@ -333,6 +337,30 @@ inline CooMatrix coo_from_entries(std::shared_ptr<Executor> exec, std::int32_t n
         exec->synchronize();
     }
     return m;
+}
+
+// io.hpp:25-28: MatrixMarket coordinate file -> canonical COO (host parse
+// with the reference's rules and messages, device assembly).
+inline CooMatrix read_matrix_market(const std::filesystem::path& path, std::shared_ptr<Executor> exec)
+{
+    lbk_mm h = nullptr;
+    const lbk_status s = lbk_mm_read(path.c_str(), &h);
+    if (s != LBK_OK) {
+        const std::string m = lbk_mm_last_error();
+        if (s == LBK_UNSUPPORTED_FORMAT) throw UnsupportedFormatError(m);
+        if (s == LBK_FORMAT_ERROR) throw FormatError(m);
+        detail::check(s);
+    }
+    int32_t nr = 0, nc = 0;
+    int64_t ne = 0;
+    const int32_t *r = nullptr, *c = nullptr;
+    const double* v = nullptr;
+    lbk_mm_info(h, &nr, &nc, &ne);
+    lbk_mm_entries(h, &r, &c, &v);
+    std::vector<MatrixEntry> entries(static_cast<std::size_t>(ne));
+    for (int64_t i = 0; i < ne; ++i) entries[i] = {r[i], c[i], v[i]};
+    lbk_mm_free(h);
+    return coo_from_entries(std::move(exec), nr, nc, entries);
 }
 
 inline std::vector<MatrixEntry> coo_to_entries(const CooMatrix& m)

@@ -109,6 +109,7 @@ def ref():
             "ref_coo_to_csr": (C.c_int, [C.c_int, C.c_int, i64, i32p, i32p, f64p, i32p, i32p, f64p]),
             "ref_csr_to_coo": (C.c_int, [C.c_int, C.c_int, i64, i32p, i32p, f64p, i32p, i32p, f64p]),
             "ref_validate": (C.c_int, [C.c_int, C.c_int, C.c_int, i64, i32p, i32p, f64p]),
+            "ref_read_mm": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64), C.c_void_p, C.c_void_p, C.c_void_p]),
             "ref_solve": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i64, i32p, i32p, f64p, f64p, f64p, C.c_int, C.c_double, C.c_int, C.c_int, f64p, C.c_int, i32p, f64p, C.POINTER(i64)]),
         }
         for name, (res, args) in sig.items():
@@ -122,6 +123,7 @@ def ref():
 class OracleError(RuntimeError):
     def __init__(self, status: int, msg: str, iteration: int = -1):
         super().__init__(f"status {status}: {msg}")
+        self.msg = msg
         self.status = status
         self.iteration = iteration
 
@@ -329,6 +331,21 @@ def ref_validate(fmt: str, nrows, ncols, ptr, cols, vals) -> int:
                               np.ascontiguousarray(ptr, np.int32),
                               np.ascontiguousarray(cols, np.int32),
                               np.ascontiguousarray(vals, np.float64))
+
+
+def ref_read_mm(path: str):
+    """The reference's read_matrix_market -> (nrows, ncols, rows, cols, vals),
+    or raises OracleError (status 8 FormatError, 11 UnsupportedFormatError)."""
+    nr, nc, nz = C.c_int(), C.c_int(), i64()
+    _chk(ref().ref_read_mm(path.encode(), C.byref(nr), C.byref(nc), C.byref(nz), None, None, None))
+    rows = np.empty(max(nz.value, 1), np.int32)
+    cols = np.empty(max(nz.value, 1), np.int32)
+    vals = np.empty(max(nz.value, 1), np.float64)
+    _chk(ref().ref_read_mm(path.encode(), C.byref(nr), C.byref(nc), C.byref(nz),
+                           rows.ctypes.data_as(C.c_void_p), cols.ctypes.data_as(C.c_void_p),
+                           vals.ctypes.data_as(C.c_void_p)))
+    k = nz.value
+    return nr.value, nc.value, rows[:k], cols[:k], vals[:k]
 
 
 @dataclass

@@ -30,6 +30,7 @@
 #include "larch/core/executor.hpp"
 #include "larch/kernels/kernels.hpp"
 #include "larch/matrix/formats.hpp"
+#include "larch/matrix/io.hpp"
 #include "larch/solver/krylov.hpp"
 
 namespace {
@@ -48,6 +49,7 @@ enum {
     ST_FORMAT = 8,
     ST_BREAKDOWN = 9,
     ST_INTEGRITY = 10,
+    ST_UNSUPPORTED = 11,
     ST_INTERNAL = 99,
 };
 
@@ -86,6 +88,9 @@ int guarded(F&& body)
     } catch (const larch::OutOfMemoryError& e) {
         g_last_error = e.what();
         return ST_OOM;
+    } catch (const larch::UnsupportedFormatError& e) {
+        g_last_error = e.what();
+        return ST_UNSUPPORTED;
     } catch (const larch::FormatError& e) {
         g_last_error = e.what();
         return ST_FORMAT;
@@ -278,6 +283,28 @@ int ref_csr_to_coo(int nrows, int ncols, std::int64_t nnz, const int* row_ptr,
         std::memcpy(rows_out, r.data(), r.size() * sizeof(int));
         std::memcpy(cols_out, c.data(), c.size() * sizeof(int));
         std::memcpy(vals_out, v.data(), v.size() * sizeof(double));
+    });
+}
+
+/// read_matrix_market(path, exec) (io.cpp:71-191) -> canonical COO.  Call
+/// with rows == nullptr first to learn the shape and nnz.
+int ref_read_mm(const char* path, int* nrows, int* ncols, std::int64_t* nnz, int* rows,
+                int* cols, double* vals)
+{
+    return guarded([&] {
+        auto exec = larch::ReferenceExecutor::create();
+        auto coo = larch::read_matrix_market(std::filesystem::path(path), exec);
+        *nrows = coo.nrows;
+        *ncols = coo.ncols;
+        *nnz = static_cast<std::int64_t>(coo.nnz());
+        if (rows) {
+            auto r = larch::array_to_host<std::int32_t>(coo.row_idx);
+            auto c = larch::array_to_host<std::int32_t>(coo.col_idx);
+            auto v = larch::array_to_host<double>(coo.vals);
+            std::memcpy(rows, r.data(), r.size() * sizeof(int));
+            std::memcpy(cols, c.data(), c.size() * sizeof(int));
+            std::memcpy(vals, v.data(), v.size() * sizeof(double));
+        }
     });
 }
 

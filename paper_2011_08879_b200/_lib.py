@@ -25,6 +25,7 @@ OUT_OF_MEMORY = 7
 FORMAT_ERROR = 8
 BREAKDOWN = 9
 BENCHMARK_INTEGRITY = 10
+UNSUPPORTED_FORMAT = 11
 CUDA_ERROR = 20
 NCCL_ERROR = 21
 INTERNAL = 99
@@ -155,6 +156,11 @@ SIGNATURES = {
     "lbk_dist_csr_destroy": (st, [vp]),
     "lbk_dist_spmv_f64": (st, [vp, vp, vp, vp, vp]),
     "lbk_dist_solve": (st, [vp, vp, vp, vp, vp, P(lbk_solver_cfg), P(lbk_solve_result), vp, i32]),
+    "lbk_mm_read": (st, [C.c_char_p, P(vp)]),
+    "lbk_mm_last_error": (C.c_char_p, []),
+    "lbk_mm_info": (st, [vp, P(i32), P(i32), P(i64)]),
+    "lbk_mm_entries": (st, [vp, P(vp), P(vp), P(vp)]),
+    "lbk_mm_free": (st, [vp]),
     "lbk_gen_stencil_nnz": (i64, [C.c_int, C.c_int]),
     "lbk_gen_stencil_csr": (st, [vp, C.c_int, C.c_int, f64, vp, vp, vp]),
     "lbk_gen_seeded_values": (None, [i64, C.c_uint64, vp]),

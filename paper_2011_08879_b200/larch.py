@@ -64,6 +64,10 @@ class FormatError(Error):
     pass
 
 
+class UnsupportedFormatError(FormatError):
+    """error.hpp:108"""
+
+
 class BreakdownError(Error):
     def __init__(self, what: str, iteration: int):
         super().__init__(what)
@@ -87,6 +91,7 @@ _STATUS = {
     L.CONFIGURATION_ERROR: ConfigurationError,
     L.OUT_OF_MEMORY: OutOfMemoryError,
     L.FORMAT_ERROR: FormatError,
+    L.UNSUPPORTED_FORMAT: UnsupportedFormatError,
     L.BENCHMARK_INTEGRITY: BenchmarkIntegrityError,
     L.CUDA_ERROR: DeviceError,
     L.NCCL_ERROR: DeviceError,
@@ -398,6 +403,39 @@ def coo_from_entries(exec: CudaExecutor, nrows: int, ncols: int, entries) -> Coo
                                          C.byref(nnz)), exec.ctx)
     k = nnz.value
     return CooMatrix(nrows, ncols, r_out[:k].clone(), c_out[:k].clone(), v_out[:k].clone(), exec)
+
+
+def read_matrix_market_entries(path: str):
+    """Host parse of a MatrixMarket coordinate file (reference io.cpp:71-191
+    acceptance rules): (nrows, ncols, rows, cols, vals) before assembly."""
+    lib = L.load()
+    h = C.c_void_p()
+    st = lib.lbk_mm_read(str(path).encode(), C.byref(h))
+    if st != L.OK:
+        msg = lib.lbk_mm_last_error().decode(errors="replace")
+        raise _STATUS.get(st, Error)(msg)
+    try:
+        nr, nc, ne = C.c_int32(), C.c_int32(), C.c_int64()
+        lib.lbk_mm_info(h, C.byref(nr), C.byref(nc), C.byref(ne))
+        pr, pc, pv = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        lib.lbk_mm_entries(h, C.byref(pr), C.byref(pc), C.byref(pv))
+        n = ne.value
+        rows = np.ctypeslib.as_array((C.c_int32 * n).from_address(pr.value)).copy() if n else \
+            np.zeros(0, np.int32)
+        cols = np.ctypeslib.as_array((C.c_int32 * n).from_address(pc.value)).copy() if n else \
+            np.zeros(0, np.int32)
+        vals = np.ctypeslib.as_array((C.c_double * n).from_address(pv.value)).copy() if n else \
+            np.zeros(0, np.float64)
+        return nr.value, nc.value, rows, cols, vals
+    finally:
+        lib.lbk_mm_free(h)
+
+
+def read_matrix_market(exec: CudaExecutor, path: str) -> CooMatrix:
+    """io.hpp:25-28 read_matrix_market: host parse + device assembly
+    (sort, duplicate sum) into canonical COO."""
+    nr, nc, rows, cols, vals = read_matrix_market_entries(path)
+    return coo_from_entries(exec, nr, nc, (rows, cols, vals))
 
 
 def coo_to_entries(m: CooMatrix):

@@ -9,7 +9,7 @@ for v in "$@"; do
   for d in ${v//,/ }; do defs="$defs -D$d"; done
   out=../../_variants/liblbk_${v//[=,]/_}.so
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 -Xcompiler -fPIC,-O3 \
-    --expt-relaxed-constexpr -I../../include $defs -shared -o $out *.cu -ldl &
+    --expt-relaxed-constexpr -I../../include $defs -shared -o $out *.cu *.cpp -ldl &
 done
 wait
 ls ../../_variants

@@ -279,6 +279,28 @@ static void test_solvers(std::shared_ptr<larch::Executor> e)
     }
 }
 
+static void test_matrix_market(std::shared_ptr<larch::Executor> e)
+{
+    // io.cpp:71-191: symmetric expansion, duplicates summed, 1-based indices
+    const char* path = "/tmp/lbk_parity_test.mtx";
+    {
+        std::FILE* f = std::fopen(path, "w");
+        std::fputs("%%MatrixMarket matrix coordinate real symmetric\n% c\n3 3 4\n1 1 2\n2 1 -1\n"
+                   "3 3 5\n2 1 0.5\n", f);
+        std::fclose(f);
+    }
+    auto M = larch::read_matrix_market(path, e);
+    CHECK((larch::coo_to_entries(M) ==
+           std::vector<larch::MatrixEntry>{{0, 0, 2.0}, {0, 1, -0.5}, {1, 0, -0.5}, {2, 2, 5.0}}));
+    {
+        std::FILE* f = std::fopen(path, "w");
+        std::fputs("%%MatrixMarket matrix coordinate complex general\n1 1 1\n1 1 1 0\n", f);
+        std::fclose(f);
+    }
+    CHECK_THROWS_AS(larch::read_matrix_market(path, e), larch::UnsupportedFormatError);
+    std::remove(path);
+}
+
 int main()
 {
     auto e = larch::create_executor(larch::ExecutorKind::cuda);
@@ -287,6 +309,7 @@ int main()
     test_random_vs_reference(e);
     test_blas1_and_errors(e);
     test_solvers(e);
+    test_matrix_market(e);
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }
