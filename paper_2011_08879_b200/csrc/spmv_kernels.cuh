@@ -185,6 +185,10 @@ inline long long stream_tile_nnz(long long nnz, long long nrows, int idx_arrays)
     return t;
 }
 
+struct int4x2 {
+    int4 a, b;
+};
+
 // first index in [lo, hi) with a[i] >= key
 template <typename P>
 __device__ __forceinline__ int lower_bound_i(P a, int lo, int hi, int key)
@@ -197,8 +201,9 @@ __device__ __forceinline__ int lower_bound_i(P a, int lo, int hi, int key)
 }
 
 // One row straight from global memory by a whole warp: rows <= 32 keep the
-// sequential order (bit-exact); longer rows use 4 independent lane partials
-// (so 4 loads per lane are in flight) and a fixed-order warp reduction.
+// sequential order (bit-exact); longer rows keep 16 loads and then 16
+// gathers per lane in flight per round, 4 lane partials and a fixed-order
+// warp reduction (deterministic).
 template <typename T>
 __device__ __forceinline__ T warp_row_global(int ks, int ke, const int* __restrict__ cols,
                                              const T* __restrict__ vals, const T* __restrict__ x)
@@ -211,19 +216,25 @@ __device__ __forceinline__ T warp_row_global(int ks, int ke, const int* __restri
         for (int k = 0; k < ke - ks; ++k) sum = add_rn(sum, __shfl_sync(0xffffffffu, p, k));
         return sum;
     }
-    T p0 = T(0), p1 = T(0), p2 = T(0), p3 = T(0);
+    // 16 independent loads (and then gathers) per lane in flight per round
+    T p[4] = {T(0), T(0), T(0), T(0)};
     int k = ks + lane;
-    for (; k + 96 < ke; k += 128) {
-        const int c0 = __ldcs(cols + k), c1 = __ldcs(cols + k + 32), c2 = __ldcs(cols + k + 64),
-                  c3 = __ldcs(cols + k + 96);
-        const T v0 = __ldcs(vals + k), v1 = __ldcs(vals + k + 32), v2 = __ldcs(vals + k + 64),
-                v3 = __ldcs(vals + k + 96);
-        p0 = add_rn(p0, mul_rn(v0, ldg_nc(x + c0)));
-        p1 = add_rn(p1, mul_rn(v1, ldg_nc(x + c1)));
-        p2 = add_rn(p2, mul_rn(v2, ldg_nc(x + c2)));
-        p3 = add_rn(p3, mul_rn(v3, ldg_nc(x + c3)));
+    for (; k + 15 * 32 < ke; k += 16 * 32) {
+        int c[16];
+        T v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            c[u] = __ldcs(cols + k + u * 32);
+            v[u] = __ldcs(vals + k + u * 32);
+        }
+        T g[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) g[u] = ldg_nc(x + c[u]);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) p[u & 3] = add_rn(p[u & 3], mul_rn(v[u], g[u]));
     }
-    for (; k < ke; k += 32) p0 = add_rn(p0, mul_rn(__ldcs(vals + k), ldg_nc(x + __ldcs(cols + k))));
+    for (; k < ke; k += 32) p[0] = add_rn(p[0], mul_rn(__ldcs(vals + k), ldg_nc(x + __ldcs(cols + k))));
+    const T p0 = p[0], p1 = p[1], p2 = p[2], p3 = p[3];
     return warp_sum(add_rn(add_rn(p0, p1), add_rn(p2, p3)));
 }
 
@@ -254,17 +265,22 @@ struct EpiPre<Epi, std::void_t<typename Epi::Pre>> {
 
 constexpr int kSeqRow = 256;  // staged rows up to this length stay bit-exact
 
-// Phase B of a staged tile, lane-per-row.  A lane owns G rows per pass
-// (rows base + g*32 + lane) and gathers the first CH entries of each of them
-// before summing, so G*CH (= 32) independent gathers per lane are in flight
-// per pass, together with the epilogue's operand loads.  Longer rows are
-// batched: the warp
-// computes the products of all of them in place (entry-parallel, 8 gathers
-// per lane in flight), then each is summed sequentially by its own lane
-// (len <= kSeqRow) or reduced by the warp.  Every row of <= kSeqRow entries
-// is summed sequentially from 0.0 in ascending k with individually rounded
-// products -- the reference's bits.  `first(q)` gives the extents of the
-// first pass (prefetched by the tile loop), `extent(r)` any row's.
+// Phase B of a staged tile.  A lane owns G rows per pass (rows base +
+// g*32 + lane).  Two modes per pass:
+//  * every row of the pass has <= 32/G entries (stencils, regular meshes):
+//    the lane gathers all entries of its G rows before summing, so 32
+//    independent gathers per lane are in flight together with the
+//    epilogue's operand loads, and across the warp the gathers hit the
+//    j-th column of consecutive rows -- coalesced like ELL;
+//  * some row is longer (power-law tiles): the warp first turns the whole
+//    entry span of the pass into products in place, entry-parallel with 16
+//    gathers per lane in flight per round (row-major order buys nothing on
+//    random columns), then every lane sums its rows from the products.
+// Every row of <= kSeqRow entries is summed sequentially from 0.0 in
+// ascending k with individually rounded products -- the reference's bits
+// (reference.cpp:82-88); longer rows are reduced by the warp.  `first(q)`
+// gives the extents of the first pass (prefetched by the tile loop),
+// `extent(r)` any row's.
 template <typename T, int G, class Epi, class First, class Ext>
 __device__ __forceinline__ void staged_rows(int rb, int re, T* sv, const int* sc,
                                             const T* __restrict__ x, const Epi& epi,
@@ -275,9 +291,9 @@ __device__ __forceinline__ void staged_rows(int rb, int re, T* sv, const int* sc
     const int lane = threadIdx.x & 31;
     for (int base = rb; base < re; base += 32 * G) {
         int o[G], len[G];
-        T v[G][CH], g[G][CH];
         typename EP::type pre[G];
-        unsigned lm = 0;
+        bool any_long = false;
+        int hi = 0;
 #pragma unroll
         for (int q = 0; q < G; ++q) {
             const int r = base + q * 32 + lane;
@@ -286,89 +302,79 @@ __device__ __forceinline__ void staged_rows(int rb, int re, T* sv, const int* sc
             if (r >= re) e = make_int2(0, 0);
             o[q] = e.x;
             len[q] = e.y;
-            lm |= __ballot_sync(0xffffffffu, e.y > CH) != 0 ? (1u << q) : 0u;
-            if (r < re) pre[q] = EP::load(epi, r);
-        }
-#pragma unroll
-        for (int q = 0; q < G; ++q) {
-#pragma unroll
-            for (int j = 0; j < CH; ++j) {
-                if (j < len[q] && len[q] <= CH) {
-                    v[q][j] = sv[o[q] + j];
-                    g[q][j] = ldg_nc(x + sc[o[q] + j]);
-                }
+            any_long |= e.y > CH;
+            if (r < re) {
+                pre[q] = EP::load(epi, r);
+                hi = hi > e.x + e.y ? hi : e.x + e.y;
             }
         }
+        if (!__any_sync(0xffffffffu, any_long)) {
+            T v[G][CH], g[G][CH];
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    if (j < len[q]) {
+                        v[q][j] = sv[o[q] + j];
+                        g[q][j] = ldg_nc(x + sc[o[q] + j]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+                const int r = base + q * 32 + lane;
+                if (r < re) {
+                    T sum = T(0);
+#pragma unroll
+                    for (int j = 0; j < CH; ++j)
+                        if (j < len[q]) sum = add_rn(sum, mul_rn(v[q][j], g[q][j]));
+                    EP::row(epi, r, sum, pre[q], acc);
+                }
+            }
+            continue;
+        }
+        // products of the pass's whole entry span, in place
+        const int lo = __shfl_sync(0xffffffffu, o[0], 0);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const int t = __shfl_xor_sync(0xffffffffu, hi, d);
+            hi = hi > t ? hi : t;
+        }
+        for (int e0 = lo; e0 < hi; e0 += 16 * 32) {
+            T gv[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int e = e0 + u * 32 + lane;
+                if (e < hi) gv[u] = ldg_nc(x + sc[e]);
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int e = e0 + u * 32 + lane;
+                if (e < hi) sv[e] = mul_rn(sv[e], gv[u]);
+            }
+        }
+        __syncwarp();
 #pragma unroll
         for (int q = 0; q < G; ++q) {
             const int r = base + q * 32 + lane;
-            if (r < re && len[q] <= CH) {
+            if (r < re && len[q] <= kSeqRow) {
                 T sum = T(0);
-#pragma unroll
-                for (int j = 0; j < CH; ++j)
-                    if (j < len[q]) sum = add_rn(sum, mul_rn(v[q][j], g[q][j]));
+                for (int k = 0; k < len[q]; ++k) sum = add_rn(sum, sv[o[q] + k]);
                 EP::row(epi, r, sum, pre[q], acc);
             }
-        }
-#pragma unroll
-        for (int q = 0; q < G; ++q) {
-            if (!(lm & (1u << q))) continue;
-            const int r = base + q * 32 + lane;
-            const bool lng = r < re && len[q] > CH;
-            // exclusive prefix of the long rows' lengths over the lanes
-            int L = lng ? len[q] : 0, inc = L;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, inc, d);
-                if (lane >= d) inc += t;
-            }
-            const int total = __shfl_sync(0xffffffffu, inc, 31);
-            // products of every long entry, in place, 8 gathers per lane in flight
-            for (int e0 = 0; e0 < total; e0 += 256) {
-                int pos[8];
-                T gv[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int e = e0 + u * 32 + lane;
-                    pos[u] = -1;
-                    // owner lane: first lane whose inclusive prefix exceeds e
-                    int lo = 0;
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        const int t = __shfl_sync(0xffffffffu, inc, lo + step - 1);
-                        if (t <= e) lo += step;
-                    }
-                    const int own_inc = __shfl_sync(0xffffffffu, inc, lo);
-                    const int own_len = __shfl_sync(0xffffffffu, L, lo);
-                    const int own_o = __shfl_sync(0xffffffffu, o[q], lo);
-                    if (e < total) {
-                        pos[u] = own_o + (e - (own_inc - own_len));
-                        gv[u] = ldg_nc(x + sc[pos[u]]);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (pos[u] >= 0) sv[pos[u]] = mul_rn(sv[pos[u]], gv[u]);
-            }
-            __syncwarp();
-            if (lng && L <= kSeqRow) {
-                T sum = T(0);
-                for (int k = 0; k < L; ++k) sum = add_rn(sum, sv[o[q] + k]);
-                EP::row(epi, r, sum, pre[q], acc);
-            }
-            unsigned m = __ballot_sync(0xffffffffu, lng && L > kSeqRow);
+            unsigned m = __ballot_sync(0xffffffffu, r < re && len[q] > kSeqRow);
             while (m) {
                 const int src = __ffs(m) - 1;
                 m &= m - 1;
                 const int ss = __shfl_sync(0xffffffffu, o[q], src);
-                const int ll = __shfl_sync(0xffffffffu, L, src);
+                const int ll = __shfl_sync(0xffffffffu, len[q], src);
                 T part = T(0);
                 for (int k = lane; k < ll; k += 32) part = add_rn(part, sv[ss + k]);
                 part = warp_sum(part);
                 if (lane == src) EP::row(epi, r, part, pre[q], acc);
             }
-            __syncwarp();
         }
+        __syncwarp();
     }
 }
 
@@ -420,12 +426,13 @@ __device__ __forceinline__ int stage_tile(int k0, int k1, long long nnz4, T* sv,
 // mk(m1, m2) -> int4 (row begin, row end, entry begin, entry end).
 // pf(bounds) issues per-lane loads for the first row pass of a tile (CSR:
 // its row_ptr entries) when the tile is staged; staged(...) gets them back.
-template <typename T, int NIDX, class M1, class M2, class Mk, class Pf, class Staged, class Wide>
+template <typename T, int NIDX, class M1, class M2, class Mk, class Pf, class Split, class Staged,
+          class Wide>
 __device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const T* vals,
                                                const int* idx0, const int* idx1,
                                                unsigned char* wbase, uint64_t* bar, M1&& meta1,
-                                               M2&& meta2, Mk&& mk, Pf&& pf, Staged&& staged,
-                                               Wide&& wide)
+                                               M2&& meta2, Mk&& mk, Pf&& pf, Split&& split,
+                                               Staged&& staged, Wide&& wide)
 {
     using Cfg = StreamCfg<T, NIDX>;
     constexpr int CAP = Cfg::kCap, NW = Cfg::kWarps, NS = Cfg::kSlots;
@@ -448,24 +455,41 @@ __device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const 
     if (t0 >= ntiles) return;
     using PfT = decltype(pf(make_int4(0, 0, 0, 0)));
     struct Q {
-        int4 bd;
+        int4 bd;    // staged part: rows [x, y), entries [z, w)
+        int4 rest;  // rows [x, y), entries [z, w) straight from global (x == y: none)
         int ka;
         bool st;
         PfT pf;
     };
-    // stage tile t (if it exists) into slot s
+    // stage tile t (if it exists) into slot s.  Only one row of a tile can
+    // overflow a slot -- the last one for a CSR plan, the first one for a
+    // COO plan (every other row lies inside the tile's T-entry window) -- so
+    // an oversize tile is split(bd) -> (staged part, rest): the rest (the
+    // giant row) goes straight from global memory.
     auto issue = [&](int t, int4 bd, int s) {
         Q q;
         q.bd = bd;
-        q.st = t < ntiles && staged_ok(bd);
+        q.rest = make_int4(0, 0, 0, 0);
+        q.st = false;
         q.ka = 0;
+        if (t < ntiles) {
+            if (staged_ok(bd)) {
+                q.st = true;
+            } else {
+                const int4x2 sp = split(bd);
+                q.bd = sp.a;
+                q.rest = sp.b;
+                q.st = q.bd.x < q.bd.y && staged_ok(q.bd);
+                if (!q.st) q.rest = bd;  // (cannot happen for CSR/COO plans)
+            }
+        }
         if (q.st) {
             fence_proxy_async_smem();
             int* i0 = slot_i0(s);
-            q.ka = stage_tile<T, NIDX>(bd.z, bd.w, nnz4, slot_v(s), i0, i0 + CAP, vals, idx0, idx1,
-                                       &bar[s], pol);
+            q.ka = stage_tile<T, NIDX>(q.bd.z, q.bd.w, nnz4, slot_v(s), i0, i0 + CAP, vals, idx0,
+                                       idx1, &bar[s], pol);
         }
-        q.pf = pf(t < ntiles ? bd : make_int4(0, 0, 0, 0));
+        q.pf = pf(q.st ? q.bd : make_int4(0, 0, 0, 0));
         return q;
     };
     // prologue: T_0 .. T_{NS-2} staged, metadata of T_{NS-1} complete and
@@ -497,9 +521,8 @@ __device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const 
         if (qc.st) {
             int* i0 = slot_i0(slot);
             staged(qc.bd, qc.ka, slot_v(slot), i0, i0 + CAP, qc.pf);
-        } else {
-            wide(qc.bd);
         }
+        if (qc.rest.x < qc.rest.y) wide(qc.rest);
         __syncwarp();
         m1a = m1b;
         m2a = m2b;
@@ -545,6 +568,10 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
                 p.v[q] = __ldg(A.row_ptr + (r < bd.y ? r : bd.y));
             }
             return p;
+        },
+        [&](int4 bd) {
+            const int ks = __ldg(A.row_ptr + bd.y - 1);  // the giant row is the last one
+            return int4x2{make_int4(bd.x, bd.y - 1, bd.z, ks), make_int4(bd.y - 1, bd.y, ks, bd.w)};
         },
         [&](int4 bd, int ka, T* sv, const int* sc, const int*, const RowPf& p) {
             staged_rows<T, G>(
@@ -616,6 +643,14 @@ __global__ void __launch_bounds__((StreamCfg<T, 2>::kThreads), 2)
                              __shfl_sync(0xffffffffu, k, 0), __shfl_sync(0xffffffffu, k, 1));
         },
         [&](int4) { return NoPf{}; },
+        [&](int4 bd) {
+            // the giant row is the first one (it holds entry t*T); the rest
+            // of the tile starts at its end
+            int ke = 0;
+            if (lane == 0) ke = lower_bound_i(A.rows, bd.z, bd.w, bd.x + 1);
+            ke = __shfl_sync(0xffffffffu, ke, 0);
+            return int4x2{make_int4(bd.x + 1, bd.y, ke, bd.w), make_int4(bd.x, bd.x + 1, bd.z, ke)};
+        },
         [&](int4 bd, int ka, T* sv, const int* sc, const int* sr, const NoPf&) {
             const int lo = bd.z - ka, hi = bd.w - ka;
             auto ext = [&](int r) {
