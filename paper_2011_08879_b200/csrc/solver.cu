@@ -33,6 +33,7 @@
 // recurrence residual sqrt(<r,r>)/||b||, and a true residual is computed
 // and must pass before convergence is declared.
 #include <chrono>
+#include <cstdlib>
 #include <vector>
 
 #include "api_guard.h"
@@ -1008,6 +1009,13 @@ struct LocalEnv {
     long long n_global() const { return n; }
     long long nnz_global() const { return nnz; }
     bool ext_x() const { return false; }
+    // single GPU: 3-5 long kernels per iteration, launch gaps are noise;
+    // LBK_SOLVER_GRAPH=1 turns capture on (tests the path)
+    bool graph_ok() const
+    {
+        const char* e = std::getenv("LBK_SOLVER_GRAPH");
+        return e && e[0] == '1';
+    }
     template <class Epi>
     void apply(const double* x, const Epi& e) { op.apply(ctx, x, e, ws); }
     template <class Op>
@@ -1059,13 +1067,23 @@ struct DistEnv {
     long long nnz_global() const { return D->nnz_global; }
     bool ext_x() const { return true; }
     bool multi() const { return comm && comm->nranks > 1; }
+    // asynchronous (NCCL) or no communicator: capturable; the thread group
+    // synchronises on the host
+    bool graph_ok() const
+    {
+        const char* e = std::getenv("LBK_SOLVER_GRAPH");
+        if (e && e[0] == '0') return false;
+        return !comm || comm->async();
+    }
+    // NCCL reduces even at one rank (keeps the captured path identical)
+    bool reduce() const { return comm && (comm->nranks > 1 || comm->async()); }
 
     template <class E>
     void finish(const E& e, int has_a, int has_b)
     {
         combine_kernel<E::NV><<<1, 32, 0, ctx->stream>>>(ws.out, has_a, has_b);
         LBK_LAUNCH_CHECK();
-        if (multi()) comm->allreduce_sum(ws.out + 16, E::NV, ctx->stream);
+        if (reduce()) comm->allreduce_sum(ws.out + 16, E::NV, ctx->stream);
         finish_kernel<E><<<1, 1, 0, ctx->stream>>>(e, ws.out + 16);
         LBK_LAUNCH_CHECK();
     }
@@ -1090,7 +1108,7 @@ struct DistEnv {
     {
         double* d = ws.out + 24;
         if (lbk_dot_f64_dev(ctx, D->n_local, b, b, d) != LBK_OK) fail(LBK_CUDA_ERROR, ctx->err);
-        if (multi()) comm->allreduce_sum(d, 1, ctx->stream);
+        if (reduce()) comm->allreduce_sum(d, 1, ctx->stream);
         double v = 0.0;
         LBK_CUDA(cudaMemcpyAsync(&v, d, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         LBK_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1266,41 +1284,81 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
 
     env.apply(x, EpiInit{b, r, p, rt, st, (bicg || cgs) ? 1 : 0, u});
 
-    // chunked launch loop; `done` is polled once per chunk
+    auto iteration = [&] {
+        if (cgs) {
+            // v and t share storage: v is dead once S3 has formed q, w
+            env.vec(OpCgsUP{u, p, q, r, st, 0.0});
+            env.apply(p, EpiCgsV{t, rt, st});
+            env.vec(OpCgsQW{q, w, u, t, st, 0.0});
+            env.apply(w, EpiCgsT{t, x, r, w, rt, st});
+            env.apply(x, EpiCgsRes{b, st});
+        } else if (!bicg) {
+            env.apply(p, EpiCgK1{q, p, st});
+            env.vec(OpCgK2{x, r, p, q, st, recurrence ? 1 : 0, 0.0});
+            if (!recurrence) {
+                env.apply(x, EpiCgK3{b, p, r, st});
+            } else {
+                env.apply(x, EpiTrueRes{b, st});
+                env.vec(OpCgP{p, r, st, 0.0});
+            }
+        } else {
+            env.apply(p, EpiBiB2{q, rt, st});
+            env.vec(OpBiB3{s, r, q, st, 0.0});
+            env.apply(s, EpiBiB4{t, s, st});
+            env.vec(OpBiB5{x, r, p, s, t, rt, st, 0.0, 0.0});
+            env.apply(x, EpiBiB6{b, p, q, r, st});
+        }
+    };
+    // Chunked launch loop; `done` is polled once per chunk.  Where the
+    // environment allows (no host-synchronous communicator), chunks after
+    // the first are captured once into a CUDA graph and replayed: the whole
+    // chunk -- SpMV/vector kernels, deferred-reduction kernels, NCCL halo
+    // send/recv on the comm stream and ncclAllReduce -- becomes one launch.
     int* done_host = reinterpret_cast<int*>(ctx->host_pinned);
     const int chunk = 16;
+    const bool use_graph = env.graph_ok();
+    cudaGraphExec_t gexec = nullptr;
     int launched = 0;
     for (;;) {
-        for (int c = 0; c < chunk && launched < limit; ++c, ++launched) {
-            if (cgs) {
-                // v and t share storage: v is dead once S3 has formed q, w
-                env.vec(OpCgsUP{u, p, q, r, st, 0.0});
-                env.apply(p, EpiCgsV{t, rt, st});
-                env.vec(OpCgsQW{q, w, u, t, st, 0.0});
-                env.apply(w, EpiCgsT{t, x, r, w, rt, st});
-                env.apply(x, EpiCgsRes{b, st});
-            } else if (!bicg) {
-                env.apply(p, EpiCgK1{q, p, st});
-                env.vec(OpCgK2{x, r, p, q, st, recurrence ? 1 : 0, 0.0});
-                if (!recurrence) {
-                    env.apply(x, EpiCgK3{b, p, r, st});
-                } else {
-                    env.apply(x, EpiTrueRes{b, st});
-                    env.vec(OpCgP{p, r, st, 0.0});
+        const int todo = limit - launched < chunk ? limit - launched : chunk;
+        if (use_graph && launched > 0 && todo == chunk) {
+            if (!gexec) {
+                // capture on a private stream (the context's stream may be the
+                // legacy default stream, which cannot be captured); the
+                // graph is then launched on the context's stream
+                cudaStream_t home = ctx->stream, cap = nullptr;
+                LBK_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+                cudaGraph_t graph = nullptr;
+                ctx->stream = cap;
+                cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed);
+                if (e == cudaSuccess) {
+                    try {
+                        for (int c = 0; c < chunk; ++c) iteration();
+                    } catch (...) {
+                        cudaStreamEndCapture(cap, &graph);
+                        ctx->stream = home;
+                        cudaStreamDestroy(cap);
+                        throw;
+                    }
+                    e = cudaStreamEndCapture(cap, &graph);
                 }
-            } else {
-                env.apply(p, EpiBiB2{q, rt, st});
-                env.vec(OpBiB3{s, r, q, st, 0.0});
-                env.apply(s, EpiBiB4{t, s, st});
-                env.vec(OpBiB5{x, r, p, s, t, rt, st, 0.0, 0.0});
-                env.apply(x, EpiBiB6{b, p, q, r, st});
+                ctx->stream = home;
+                cudaStreamDestroy(cap);
+                LBK_CUDA(e);
+                LBK_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
+                cudaGraphDestroy(graph);
             }
+            LBK_CUDA(cudaGraphLaunch(gexec, ctx->stream));
+        } else {
+            for (int c = 0; c < todo; ++c) iteration();
         }
+        launched += todo;
         LBK_CUDA(cudaMemcpyAsync(done_host, &st->done, sizeof(int), cudaMemcpyDeviceToHost,
                                  ctx->stream));
         LBK_CUDA(cudaStreamSynchronize(ctx->stream));
         if (*done_host || launched >= limit) break;
     }
+    if (gexec) cudaGraphExecDestroy(gexec);
     finish_solve(ctx, env, st, hist, x, x_user, n, limit, cfg, res, history, hist_cap, ev0, ev1);
 }
 

@@ -136,3 +136,13 @@ def test_nccl_single_rank(O, lk):
     x = torch.zeros(A.nrows, dtype=torch.float64, device="cuda")
     r = M.solve(comm, torch.from_numpy(b).cuda(), x, lk.SolverConfig(kind="cg", rel_tol=1e-8))
     assert abs(r.iterations - 41) <= 1
+    # chunks after the first run as a captured CUDA graph (NCCL allreduce
+    # inside); the 32^3 solve (81 iterations) replays it several times
+    A = O.stencil("7pt", 32)
+    b = O.spmv_csr(A, np.ones(A.nrows))
+    m = D.DistMap(A.nrows, 1, 0, A.row_ptr, A.cols)
+    D.exchange_requests_local([m])
+    M = D.DistCsrMatrix(ex, m, A.row_ptr, A.vals, A.nnz)
+    x = torch.zeros(A.nrows, dtype=torch.float64, device="cuda")
+    r = M.solve(comm, torch.from_numpy(b).cuda(), x, lk.SolverConfig(kind="cg", rel_tol=1e-8))
+    assert abs(r.iterations - 81) <= 1 and r.converged

@@ -263,3 +263,19 @@ def test_gmres_fixed_iters(R, ex, lk):
                  gmres_restart=7)
     assert r.iterations == rr.iterations == 50
     assert len(r.residual_history) == 51
+
+
+@pytest.mark.parametrize("kind", ["cg", "bicgstab", "cgs"])
+def test_graph_captured_chunks_identical(O, ex, lk, kind, monkeypatch):
+    """Chunks after the first replayed as one CUDA graph give the same
+    iterations, history and x, bit for bit."""
+    A = O.stencil("7pt", 24, 0.5 if kind != "cg" else 0.0)
+    b = O.spmv_csr(A, O.seeded_values(A.nrows, 11))
+    M = up(lk, ex, A)
+    monkeypatch.setenv("LBK_SOLVER_GRAPH", "0")
+    r0, x0 = solve(lk, ex, M, b, kind=kind, rel_tol=1e-8, max_iters=20000)
+    monkeypatch.setenv("LBK_SOLVER_GRAPH", "1")
+    r1, x1 = solve(lk, ex, M, b, kind=kind, rel_tol=1e-8, max_iters=20000)
+    assert r0.iterations == r1.iterations and r0.iterations > 32
+    assert r0.residual_history == r1.residual_history
+    assert np.array_equal(x0, x1) and r0.flop_count == r1.flop_count
