@@ -812,6 +812,67 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Lane-per-row variant: consecutive lanes own consecutive rows, so the
+// column-j loads of a warp are one contiguous 128 B (indices) / 256 B
+// (values) run and the x gathers of a stencil hit 2 lines -- about half the
+// L1 wavefronts of the 4-rows-per-thread kernel, whose gathers stride 32 B
+// across lanes.  8 columns' loads and then 8 gathers per thread in flight.
+template <typename T, class Epi, bool IS_ELL>
+__global__ void __launch_bounds__(256)
+    sliced_lane_kernel(int nrows, int S, const int* __restrict__ slice_sets, int ell_width,
+                       const int* __restrict__ cols, const T* __restrict__ vals,
+                       const T* __restrict__ x, Epi epi, RedWs ws)
+{
+    constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
+    constexpr int U = 8;
+    __shared__ double red_sh[32 * NV];
+    if (epi.skip()) return;
+    double acc[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    for (long long rr = blockIdx.x * (long long)blockDim.x + threadIdx.x; rr < nrows;
+         rr += (long long)gridDim.x * blockDim.x) {
+        const int r = static_cast<int>(rr);
+        long long base;
+        int len;
+        if constexpr (IS_ELL) {
+            base = r;
+            len = ell_width;
+        } else {
+            const int sl = r / S;
+            const int a = __ldg(slice_sets + sl), b = __ldg(slice_sets + sl + 1);
+            base = static_cast<long long>(a) * S + (r - sl * S);
+            len = b - a;
+        }
+        const long long pitch = S;
+        T sum = T(0);
+        for (int j0 = 0; j0 < len; j0 += U) {
+            int c[U];
+            T v[U], g[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                c[u] = -1;
+                if (j0 + u < len) {
+                    const long long o = base + (j0 + u) * pitch;
+                    c[u] = __ldcs(cols + o);
+                    v[u] = __ldcs(vals + o);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) g[u] = c[u] >= 0 ? ldg_nc(x + c[u]) : T(0);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (c[u] >= 0) sum = add_rn(sum, mul_rn(v[u], g[u]));
+        }
+        epi.row(r, sum, acc);
+    }
+    if constexpr (Epi::NV > 0) {
+        block_sum<NV>(acc, threadIdx.x, blockDim.x, red_sh);
+        grid_reduce_finish<NV>(acc, ws, threadIdx.x, blockDim.x, red_sh,
+                               [&](const double* tot) { epi.finish(tot); });
+    }
+}
+
 // Scalar fallback (unaligned / odd slice heights): thread per row.
 template <typename T, class Epi, bool IS_ELL>
 __global__ void __launch_bounds__(256)

@@ -165,8 +165,27 @@ void launch_sliced(lbk_ctx ctx, int nrows, int S, const int* slice_sets, int wid
     const int pitch = IS_ELL ? static_cast<int>(ell_stride) : S;
     const bool quad_ok = aligned16(cols) && aligned16(vals) && pitch % 4 == 0 &&
                          (!IS_ELL || ell_stride >= ((static_cast<long long>(nrows) + 3) & ~3LL));
-    const long long units = quad_ok ? (static_cast<long long>(nrows) + 3) / 4 : nrows;
-    if (quad_ok) {
+    static const int algo = [] {
+        const char* e = std::getenv("LBK_SLICED");
+        // quad (4 rows per thread, 128-bit loads) is the default; lane-per-row
+        // and scalar row kernels measured within noise of it on cfg2
+        if (e && std::strcmp(e, "lane") == 0) return 0;
+        if (e && std::strcmp(e, "row") == 0) return 2;
+        return 1;
+    }();
+    if (algo == 0) {
+        auto k = sliced_lane_kernel<T, Epi, IS_ELL>;
+        static int bps = blocks_per_sm(k, 256, 0);
+        long long want = (static_cast<long long>(nrows) + 255) / 256;
+        long long cap = static_cast<long long>(ctx->num_sms) * bps;
+        if (Epi::NV > 0 && cap > kRedMaxBlocks) cap = kRedMaxBlocks;
+        int grid = static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap);
+        k<<<grid, 256, 0, ctx->stream>>>(nrows, pitch, slice_sets, width, cols, vals, x, epi, ws);
+        LBK_LAUNCH_CHECK();
+        return;
+    }
+    const long long units = quad_ok && algo == 1 ? (static_cast<long long>(nrows) + 3) / 4 : nrows;
+    if (quad_ok && algo == 1) {
         auto k = sliced_quad_kernel<T, Epi, IS_ELL>;
         static int bps = blocks_per_sm(k, 256, 0);
         long long want = (units + 255) / 256, cap = static_cast<long long>(ctx->num_sms) * bps;
