@@ -194,6 +194,9 @@ void build_sub(lbk_ctx ctx, SubCsr& S, const std::vector<int>& rows, const int32
         rp[i + 1] = static_cast<int>(cols.size());
     }
     S.nrows = static_cast<int>(rows.size());
+    S.row_off = rows.empty() ? 0 : rows.front();
+    for (size_t i = 1; i < rows.size() && S.row_off >= 0; ++i)
+        if (rows[i] != rows[i - 1] + 1) S.row_off = -1;
     S.ncols = ncols;
     S.nnz = static_cast<long long>(cols.size());
     S.row_ptr.alloc(rp.size() * 4);

@@ -74,6 +74,8 @@ struct SubCsr {
     long long nnz = 0;
     DevArr row_ptr, cols, vals, row_map, plan;
     int ntiles = 0;
+    int row_off = -1;  // >= 0: rows are contiguous from row_off (no row_map)
+    const int* map() const { return row_off >= 0 ? nullptr : row_map.as<int>(); }
     CsrView<double> view() const
     {
         return CsrView<double>{nrows, ncols, nnz, row_ptr.as<int>(), cols.as<int>(),
@@ -82,26 +84,30 @@ struct SubCsr {
 };
 
 // Epilogue adaptor: sub-matrix row -> local row.
+// A contiguous row subset (the interior rows of a row-block partition of a
+// banded matrix) is mapped by an offset instead of a lookup (map == null).
 template <class Epi>
 struct MappedEpi {
     static constexpr int NV = Epi::NV;
     Epi e;
     const int* __restrict__ map;
+    int off;
     struct Pre {
         int r;
         typename EpiPre<Epi>::type p;
     };
+    __device__ int local(int r) const { return map ? __ldg(map + r) : r + off; }
     __device__ bool skip() const { return e.skip(); }
     __device__ Pre pre(int r) const
     {
-        const int m = __ldg(map + r);
+        const int m = local(r);
         return {m, EpiPre<Epi>::load(e, m)};
     }
     __device__ void row_pre(int, double s, const Pre& p, double* acc) const
     {
         EpiPre<Epi>::row(e, p.r, s, p.p, acc);
     }
-    __device__ void row(int r, double s, double* acc) const { e.row(__ldg(map + r), s, acc); }
+    __device__ void row(int r, double s, double* acc) const { e.row(local(r), s, acc); }
     __device__ void finish(const double* t) const { e.finish(t); }
 };
 
@@ -148,12 +154,12 @@ void dist_apply(lbk_ctx ctx, lbk_dist_csr_s* D, Comm* comm, double* x_ext, const
         }
     }
     if (D->interior.nrows > 0)
-        launch_csr<double>(ctx, D->interior.view(), x_ext, MappedEpi<Epi>{epi, D->interior.row_map.as<int>()},
-                           ws_a);
+        launch_csr<double>(ctx, D->interior.view(), x_ext,
+                           MappedEpi<Epi>{epi, D->interior.map(), D->interior.row_off}, ws_a);
     if (xchg && comm->async()) LBK_CUDA(cudaStreamWaitEvent(ctx->stream, D->ev_recv, 0));
     if (D->boundary.nrows > 0)
-        launch_csr<double>(ctx, D->boundary.view(), x_ext, MappedEpi<Epi>{epi, D->boundary.row_map.as<int>()},
-                           ws_b);
+        launch_csr<double>(ctx, D->boundary.view(), x_ext,
+                           MappedEpi<Epi>{epi, D->boundary.map(), D->boundary.row_off}, ws_b);
 }
 
 }  // namespace lbk
