@@ -146,3 +146,28 @@ def test_nccl_single_rank(O, lk):
     x = torch.zeros(A.nrows, dtype=torch.float64, device="cuda")
     r = M.solve(comm, torch.from_numpy(b).cuda(), x, lk.SolverConfig(kind="cg", rel_tol=1e-8))
     assert abs(r.iterations - 81) <= 1 and r.converged
+
+
+@pytest.mark.parametrize("kind,P", [("cgs", 2), ("gmres", 3)])
+def test_dist_cgs_gmres(O, lk, kind, P):
+    """The other solvers run unchanged on the distributed environment."""
+    A = O.stencil("7pt", 14, 0.5)
+    b = O.spmv_csr(A, O.seeded_values(A.nrows, 11))
+    exs, mats, comms = build(O, lk, A, P)
+    from paper_2011_08879_b200 import dist as D
+    rng = [D.part_range(A.nrows, P, r) for r in range(P)]
+    bs = [torch.from_numpy(b[lo:hi].copy()).cuda() for lo, hi in rng]
+    xs = [torch.zeros(hi - lo, dtype=torch.float64, device="cuda") for lo, hi in rng]
+    torch.cuda.synchronize()
+    cfg = lk.SolverConfig(kind=kind, rel_tol=1e-8, max_iters=20000, gmres_restart=20)
+    res = run_threads(P, lambda r: mats[r].solve(comms[r], bs[r], xs[r], cfg))
+    torch.cuda.synchronize()
+    assert all(r.iterations == res[0].iterations for r in res)
+    if O.ref_available():
+        rr = O.ref_solve(A, b, kind, rel_tol=1e-8, max_iters=20000, restart=20)
+        rp = O.ref_solve(A, b, kind, rel_tol=1e-8, max_iters=20000, restart=20, exec_kind=1,
+                         workers=8)
+        assert abs(res[0].iterations - rr.iterations) <= max(1, abs(rp.iterations - rr.iterations))
+    x = np.concatenate([t.cpu().numpy() for t in xs])
+    assert res[0].converged
+    assert np.max(np.abs(O.spmv_csr(A, x) - b)) <= 1e-7 * np.max(np.abs(b))
