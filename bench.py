@@ -448,6 +448,7 @@ def run_cg(ex, world: int, rank: int, local_rank: int, force_dist: bool = False)
                                                      residual_mode=mode))
             cg[mode] = {"iterations": r.iterations, "final_rel_residual": r.final_rel_residual,
                         "seconds": r.elapsed, "iters_per_s": r.iterations / r.elapsed,
+                        "flop_count": r.flop_count,
                         "gflops_ref_model": r.flop_count / r.elapsed / 1e9}
         del A4, ones, b, xs
         torch.cuda.empty_cache()
@@ -463,6 +464,7 @@ def run_cg(ex, world: int, rank: int, local_rank: int, force_dist: bool = False)
                                "iterations": r.iterations,
                                "final_rel_residual": r.final_rel_residual, "seconds": r.elapsed,
                                "iters_per_s": r.iterations / r.elapsed,
+                               "flop_count": r.flop_count,
                                "gflops_ref_model": r.flop_count / r.elapsed / 1e9}
         return cg
     # distributed: this rank's rows of the same matrix
@@ -493,7 +495,7 @@ def run_cg(ex, world: int, rank: int, local_rank: int, force_dist: bool = False)
                                                      residual_mode=mode))
         el = tmax(r.elapsed)
         cg[mode] = {"iterations": r.iterations, "final_rel_residual": r.final_rel_residual,
-                    "seconds": el, "iters_per_s": r.iterations / el,
+                    "seconds": el, "iters_per_s": r.iterations / el, "flop_count": r.flop_count,
                     "gflops_ref_model": r.flop_count / el / 1e9}
     return cg
 
@@ -564,6 +566,8 @@ def main() -> None:
     ap.add_argument("--no-cg", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-formats", action="store_true")
+    ap.add_argument("--report-dir", default=None,
+                    help="also write BenchRecord json/csv/svg (reference schema) here")
     ap.add_argument("--no-cfg3", action="store_true")
     ap.add_argument("--cg-dist", action="store_true",
                     help="use the row-partitioned solver for the CG leg even at N = 1")
