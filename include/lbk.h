@@ -72,6 +72,10 @@ lbk_status lbk_sync(lbk_ctx ctx);
 lbk_status lbk_ctx_info(lbk_ctx ctx, int* device, int* num_sms,
                         size_t* arena_capacity, size_t* arena_used);
 lbk_status lbk_ctx_set_arena_capacity(lbk_ctx ctx, size_t bytes);
+/* L2 access-policy window over the SpMV's gathered vector x (persisting,
+ * per launch via cudaLaunchAttributeAccessPolicyWindow).  Default off
+ * (env LBK_L2_PERSIST=1 turns it on at context creation). */
+lbk_status lbk_ctx_set_l2_persist(lbk_ctx ctx, int on);
 /* Executor::raw_alloc / raw_free (executor.cpp:254-279): device memory,
  * 256-B aligned, LBK_OUT_OF_MEMORY past the arena capacity. */
 lbk_status lbk_alloc(lbk_ctx ctx, size_t bytes, void** out);

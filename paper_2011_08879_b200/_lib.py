@@ -95,6 +95,7 @@ SIGNATURES = {
     "lbk_sync": (st, [vp]),
     "lbk_ctx_info": (st, [vp, P(C.c_int), P(C.c_int), P(C.c_size_t), P(C.c_size_t)]),
     "lbk_ctx_set_arena_capacity": (st, [vp, C.c_size_t]),
+    "lbk_ctx_set_l2_persist": (st, [vp, C.c_int]),
     "lbk_alloc": (st, [vp, C.c_size_t, P(vp)]),
     "lbk_free": (st, [vp, vp, C.c_size_t]),
     "lbk_memcpy_h2d": (st, [vp, vp, vp, C.c_size_t]),

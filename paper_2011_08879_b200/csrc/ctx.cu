@@ -1,5 +1,6 @@
 // ctx.cu -- context, arena accounting, copies (the Executor seam:
 // reference include/larch/core/executor.hpp:130-170, device_array.cpp:144-263).
+#include <cstdlib>
 #include <cstring>
 
 #include "api_guard.h"
@@ -86,6 +87,16 @@ static lbk_status ctx_create_impl(int device, void* stream, bool own, lbk_ctx* o
         need(major == 10, LBK_DISPATCH_ERROR,
              "lbk kernels are built for sm_100a (B200); device has compute capability " +
                  std::to_string(major) + ".x");
+        {
+            int win = 0, lim = 0;
+            cudaDeviceGetAttribute(&win, cudaDevAttrMaxAccessPolicyWindowSize, device);
+            cudaDeviceGetAttribute(&lim, cudaDevAttrMaxPersistingL2CacheSize, device);
+            ctx->persist_max = static_cast<size_t>(win < lim ? win : lim);
+            const char* e = std::getenv("LBK_L2_PERSIST");
+            ctx->l2_persist = (e && e[0] == '1') ? 1 : 0;
+            if (ctx->l2_persist && ctx->persist_max)
+                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(lim));
+        }
         if (own) {
             LBK_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
             ctx->own_stream = true;
@@ -124,6 +135,19 @@ lbk_status lbk_ctx_set_stream(lbk_ctx ctx, void* stream)
             ctx->own_stream = false;
         }
         ctx->stream = static_cast<cudaStream_t>(stream);
+    });
+}
+
+lbk_status lbk_ctx_set_l2_persist(lbk_ctx ctx, int on)
+{
+    if (!ctx) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        ctx->l2_persist = on ? 1 : 0;
+        if (on && ctx->persist_max) {
+            int lim = 0;
+            LBK_CUDA(cudaDeviceGetAttribute(&lim, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
+            LBK_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(lim)));
+        }
     });
 }
 

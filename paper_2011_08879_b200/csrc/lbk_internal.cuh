@@ -60,6 +60,11 @@ struct lbk_ctx_s {
     lbk::DevBuf scratch;
     lbk::DevBuf red;
     double* host_pinned = nullptr;  // 64 doubles for synchronous readbacks
+    // L2 access-policy window on the gathered vector x (per launch,
+    // cudaLaunchAttributeAccessPolicyWindow): persisting hits for x, streaming
+    // misses.  0 off, 1 on; persist_max = the device's window / carve-out.
+    int l2_persist = 0;
+    size_t persist_max = 0;
 };
 
 namespace lbk {

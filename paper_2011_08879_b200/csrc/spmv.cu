@@ -130,7 +130,7 @@ void run_ell(lbk_ctx ctx, const lbk_ell* A, const T* x, const Epi& epi, lbk_dtyp
          "spmv_ell: need width >= 0 and stride >= nrows");
     if (A->nrows == 0) return;
     launch_sliced<T, Epi, true>(ctx, A->nrows, 0, nullptr, A->width, A->stride, A->col_idx,
-                                static_cast<const T*>(A->vals), x, epi, RedWs{});
+                                static_cast<const T*>(A->vals), x, epi, RedWs{}, A->ncols);
 }
 
 template <typename T, class Epi>
@@ -143,7 +143,8 @@ void run_sellp(lbk_ctx ctx, const lbk_sellp* A, const T* x, const Epi& epi, lbk_
          "spmv_sellp: nslices != ceil(nrows / slice_size)");
     if (A->nrows == 0) return;
     launch_sliced<T, Epi, false>(ctx, A->nrows, A->slice_size, A->slice_sets, 0, 0,
-                                 A->col_idx, static_cast<const T*>(A->vals), x, epi, RedWs{});
+                                 A->col_idx, static_cast<const T*>(A->vals), x, epi, RedWs{},
+                                 A->ncols);
 }
 
 }  // namespace

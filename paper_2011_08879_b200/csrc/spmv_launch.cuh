@@ -77,6 +77,35 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Launch with, when the context asks for it, an L2 access-policy window
+// over the gathered vector x (persisting) -- the matrix streams already
+// carry evict-first hints, so x keeps its place in L2 between launches.
+template <typename... KArgs, typename... Args>
+void launch_k(lbk_ctx ctx, void (*kernel)(KArgs...), int grid, int block, size_t smem,
+              const void* x, size_t x_bytes, Args&&... args)
+{
+    if (!ctx->l2_persist || !x || !ctx->persist_max) {
+        kernel<<<grid, block, smem, ctx->stream>>>(std::forward<Args>(args)...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    const size_t nb = x_bytes < ctx->persist_max ? x_bytes : ctx->persist_max;
+    attr[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(x);
+    attr[0].val.accessPolicyWindow.num_bytes = nb;
+    attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LBK_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 template <class K>
 int blocks_per_sm(K kernel, int threads, size_t smem)
 {
@@ -106,7 +135,7 @@ void stream_launch(lbk_ctx ctx, K kernel, const View& A, const T* x, const Epi& 
     if (cap > kRedMaxBlocks) cap = kRedMaxBlocks;
     const long long want = (A.ntiles + Cfg::kWarps - 1) / Cfg::kWarps;
     const int grid = static_cast<int>(want < cap ? want : cap);
-    kernel<<<grid, Cfg::kThreads, smem, ctx->stream>>>(A, x, epi, ws);
+    launch_k(ctx, kernel, grid, Cfg::kThreads, smem, x, size_t(A.ncols) * sizeof(T), A, x, epi, ws);
     LBK_LAUNCH_CHECK();
 }
 
@@ -160,7 +189,7 @@ void launch_coo(lbk_ctx ctx, CooView<T> A, const T* x, const Epi& epi, RedWs ws)
 template <typename T, class Epi, bool IS_ELL>
 void launch_sliced(lbk_ctx ctx, int nrows, int S, const int* slice_sets, int width,
                    long long ell_stride, const int* cols, const T* vals, const T* x,
-                   const Epi& epi, RedWs ws)
+                   const Epi& epi, RedWs ws, long long x_len = 0)
 {
     const int pitch = IS_ELL ? static_cast<int>(ell_stride) : S;
     const bool quad_ok = aligned16(cols) && aligned16(vals) && pitch % 4 == 0 &&
@@ -180,7 +209,8 @@ void launch_sliced(lbk_ctx ctx, int nrows, int S, const int* slice_sets, int wid
         long long cap = static_cast<long long>(ctx->num_sms) * bps;
         if (Epi::NV > 0 && cap > kRedMaxBlocks) cap = kRedMaxBlocks;
         int grid = static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap);
-        k<<<grid, 256, 0, ctx->stream>>>(nrows, pitch, slice_sets, width, cols, vals, x, epi, ws);
+        launch_k(ctx, k, grid, 256, 0, x, size_t(x_len) * sizeof(T), nrows, pitch, slice_sets, width,
+                 cols, vals, x, epi, ws);
         LBK_LAUNCH_CHECK();
         return;
     }
@@ -190,13 +220,15 @@ void launch_sliced(lbk_ctx ctx, int nrows, int S, const int* slice_sets, int wid
         static int bps = blocks_per_sm(k, 256, 0);
         long long want = (units + 255) / 256, cap = static_cast<long long>(ctx->num_sms) * bps;
         int grid = static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap);
-        k<<<grid, 256, 0, ctx->stream>>>(nrows, pitch, slice_sets, width, cols, vals, x, epi, ws);
+        launch_k(ctx, k, grid, 256, 0, x, size_t(x_len) * sizeof(T), nrows, pitch, slice_sets, width,
+                 cols, vals, x, epi, ws);
     } else {
         auto k = sliced_row_kernel<T, Epi, IS_ELL>;
         static int bps = blocks_per_sm(k, 256, 0);
         long long want = (units + 255) / 256, cap = static_cast<long long>(ctx->num_sms) * bps;
         int grid = static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap);
-        k<<<grid, 256, 0, ctx->stream>>>(nrows, pitch, slice_sets, width, cols, vals, x, epi, ws);
+        launch_k(ctx, k, grid, 256, 0, x, size_t(x_len) * sizeof(T), nrows, pitch, slice_sets, width,
+                 cols, vals, x, epi, ws);
     }
     LBK_LAUNCH_CHECK();
 }
