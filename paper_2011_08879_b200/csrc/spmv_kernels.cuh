@@ -278,13 +278,15 @@ constexpr int kSeqRow = 256;  // staged rows up to this length stay bit-exact
 //    random columns), then every lane sums its rows from the products.
 // Every row of <= kSeqRow entries is summed sequentially from 0.0 in
 // ascending k with individually rounded products -- the reference's bits
-// (reference.cpp:82-88); longer rows are reduced by the warp.  `first(q)`
-// gives the extents of the first pass (prefetched by the tile loop),
-// `extent(r)` any row's.
-template <typename T, int G, class Epi, class First, class Ext>
+// (reference.cpp:82-88); longer rows are reduced by the warp.
+// `starts(base, s)` fills s[q] (q = 0..G) with the slot offset where row
+// base + q*32 + lane starts (the tile's entry end for rows >= re); a row's
+// extent is then its start and the next row's start, taken from the
+// neighbouring lane -- one lookup per row instead of two.
+template <typename T, int G, class Epi, class Starts>
 __device__ __forceinline__ void staged_rows(int rb, int re, T* sv, const int* sc,
                                             const T* __restrict__ x, const Epi& epi,
-                                            double* acc, First&& first, Ext&& extent)
+                                            double* acc, Starts&& starts)
 {
     using EP = EpiPre<Epi>;
     constexpr int CH = 32 / G;
@@ -294,11 +296,17 @@ __device__ __forceinline__ void staged_rows(int rb, int re, T* sv, const int* sc
         typename EP::type pre[G];
         bool any_long = false;
         int hi = 0;
+        int st[G + 1];
+        starts(base, st);
 #pragma unroll
         for (int q = 0; q < G; ++q) {
             const int r = base + q * 32 + lane;
-            int2 e = base == rb ? first(q) : make_int2(0, 0);
-            if (base != rb && r < re) e = extent(r);
+            // next row's start: the neighbouring lane's (lane 31: lane 0 of
+            // the next group, or of the group after the pass)
+            int nx = __shfl_sync(0xffffffffu, st[q], (lane + 1) & 31);
+            const int wrap = __shfl_sync(0xffffffffu, st[q + 1], 0);
+            if (lane == 31) nx = wrap;
+            int2 e = make_int2(st[q], nx - st[q]);
             if (r >= re) e = make_int2(0, 0);
             o[q] = e.x;
             len[q] = e.y;
@@ -574,23 +582,18 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
             return int4x2{make_int4(bd.x, bd.y - 1, bd.z, ks), make_int4(bd.y - 1, bd.y, ks, bd.w)};
         },
         [&](int4 bd, int ka, T* sv, const int* sc, const int*, const RowPf& p) {
-            staged_rows<T, G>(
-                bd.x, bd.y, sv, sc, x, epi, acc,
-                [&](int q) {
-                    // end of row (q, lane) = start held by lane + 1 (lane 31:
-                    // lane 0 of group q + 1)
-                    int nx = __shfl_sync(0xffffffffu, p.v[q], (lane + 1) & 31);
-                    int wrap = 0;
+            staged_rows<T, G>(bd.x, bd.y, sv, sc, x, epi, acc, [&](int base, int* st) {
+                if (base == bd.x) {  // prefetched when the tile was staged
 #pragma unroll
-                    for (int u = 0; u <= G; ++u)
-                        if (u == q + 1) wrap = __shfl_sync(0xffffffffu, p.v[u], 0);
-                    if (lane == 31) nx = wrap;
-                    return make_int2(p.v[q] - ka, nx - p.v[q]);
-                },
-                [&](int r) {
-                    const int rs = __ldg(A.row_ptr + r);
-                    return make_int2(rs - ka, __ldg(A.row_ptr + r + 1) - rs);
-                });
+                    for (int q = 0; q <= G; ++q) st[q] = p.v[q] - ka;
+                } else {
+#pragma unroll
+                    for (int q = 0; q <= G; ++q) {
+                        const int r = base + q * 32 + lane;
+                        st[q] = __ldg(A.row_ptr + (r < bd.y ? r : bd.y)) - ka;
+                    }
+                }
+            });
         },
         [&](int4 bd) {
             for (int r = bd.x; r < bd.y; ++r) {
@@ -653,17 +656,17 @@ __global__ void __launch_bounds__((StreamCfg<T, 2>::kThreads), 2)
         },
         [&](int4 bd, int ka, T* sv, const int* sc, const int* sr, const NoPf&) {
             const int lo = bd.z - ka, hi = bd.w - ka;
-            auto ext = [&](int r) {
-                const int rs = lower_bound_i(sr, lo, hi, r);
-                return make_int2(rs, lower_bound_i(sr, rs, hi, r + 1) - rs);
-            };
-            staged_rows<T, G>(
-                bd.x, bd.y, sv, sc, x, epi, acc,
-                [&](int q) {
-                    const int r = bd.x + q * 32 + lane;
-                    return r < bd.y ? ext(r) : make_int2(0, 0);
-                },
-                ext);
+            staged_rows<T, G>(bd.x, bd.y, sv, sc, x, epi, acc, [&](int base, int* st) {
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    const int r = base + q * 32 + lane;
+                    st[q] = r < bd.y ? lower_bound_i(sr, lo, hi, r) : hi;
+                }
+                // start of the row after the pass (used by lane 31 of the last
+                // group): the tile's end when the pass reaches it
+                const int rn = base + G * 32;
+                st[G] = rn < bd.y ? lower_bound_i(sr, lo, hi, rn) : hi;
+            });
         },
         [&](int4 bd) {
             for (int r = bd.x; r < bd.y; ++r) {
