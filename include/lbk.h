@@ -85,6 +85,9 @@ lbk_status lbk_free(lbk_ctx ctx, void* ptr, size_t bytes);
 lbk_status lbk_memcpy_h2d(lbk_ctx ctx, void* dst, const void* src, size_t bytes);
 lbk_status lbk_memcpy_d2h(lbk_ctx ctx, void* dst, const void* src, size_t bytes);
 lbk_status lbk_memcpy_d2d(lbk_ctx ctx, void* dst, const void* src, size_t bytes);
+/* explicit GPU -> GPU copy (NVLink P2P where enabled), stream-ordered */
+lbk_status lbk_memcpy_peer(lbk_ctx ctx, void* dst, int dst_device, const void* src,
+                           int src_device, size_t bytes);
 
 /* ---------------------------------------------------------- matrices */
 /* CsrMatrix (formats.hpp:65-76).  `tile_rows` is an optional load-balance
@@ -155,14 +158,20 @@ lbk_status lbk_spmv_coo_f64(lbk_ctx, const lbk_coo* A, const double* x, double* 
 lbk_status lbk_spmv_coo_f32(lbk_ctx, const lbk_coo* A, const float* x, float* y);
 lbk_status lbk_spmv_coo_adv_f64(lbk_ctx, double alpha, const lbk_coo* A,
                                 const double* x, double beta, double* y);
+lbk_status lbk_spmv_coo_adv_f32(lbk_ctx, float alpha, const lbk_coo* A,
+                                const float* x, float beta, float* y);
 lbk_status lbk_spmv_ell_f64(lbk_ctx, const lbk_ell* A, const double* x, double* y);
 lbk_status lbk_spmv_ell_f32(lbk_ctx, const lbk_ell* A, const float* x, float* y);
 lbk_status lbk_spmv_ell_adv_f64(lbk_ctx, double alpha, const lbk_ell* A,
                                 const double* x, double beta, double* y);
+lbk_status lbk_spmv_ell_adv_f32(lbk_ctx, float alpha, const lbk_ell* A,
+                                const float* x, float beta, float* y);
 lbk_status lbk_spmv_sellp_f64(lbk_ctx, const lbk_sellp* A, const double* x, double* y);
 lbk_status lbk_spmv_sellp_f32(lbk_ctx, const lbk_sellp* A, const float* x, float* y);
 lbk_status lbk_spmv_sellp_adv_f64(lbk_ctx, double alpha, const lbk_sellp* A,
                                   const double* x, double beta, double* y);
+lbk_status lbk_spmv_sellp_adv_f32(lbk_ctx, float alpha, const lbk_sellp* A,
+                                  const float* x, float beta, float* y);
 
 /* Load-balance plans (Ginkgo's "strategy" objects; the reference has none).
  * CSR: nnz-balanced row tiles; tile_rows needs lbk_csr_plan_size() int32s.

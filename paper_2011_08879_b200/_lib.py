@@ -101,6 +101,7 @@ SIGNATURES = {
     "lbk_memcpy_h2d": (st, [vp, vp, vp, C.c_size_t]),
     "lbk_memcpy_d2h": (st, [vp, vp, vp, C.c_size_t]),
     "lbk_memcpy_d2d": (st, [vp, vp, vp, C.c_size_t]),
+    "lbk_memcpy_peer": (st, [vp, vp, C.c_int, vp, C.c_int, C.c_size_t]),
     "lbk_spmv_csr_f64": (st, [vp, P(lbk_csr), vp, vp]),
     "lbk_spmv_csr_f32": (st, [vp, P(lbk_csr), vp, vp]),
     "lbk_spmv_csr_adv_f64": (st, [vp, f64, P(lbk_csr), vp, f64, vp]),
@@ -108,12 +109,15 @@ SIGNATURES = {
     "lbk_spmv_coo_f64": (st, [vp, P(lbk_coo), vp, vp]),
     "lbk_spmv_coo_f32": (st, [vp, P(lbk_coo), vp, vp]),
     "lbk_spmv_coo_adv_f64": (st, [vp, f64, P(lbk_coo), vp, f64, vp]),
+    "lbk_spmv_coo_adv_f32": (st, [vp, f32, P(lbk_coo), vp, f32, vp]),
     "lbk_spmv_ell_f64": (st, [vp, P(lbk_ell), vp, vp]),
     "lbk_spmv_ell_f32": (st, [vp, P(lbk_ell), vp, vp]),
     "lbk_spmv_ell_adv_f64": (st, [vp, f64, P(lbk_ell), vp, f64, vp]),
+    "lbk_spmv_ell_adv_f32": (st, [vp, f32, P(lbk_ell), vp, f32, vp]),
     "lbk_spmv_sellp_f64": (st, [vp, P(lbk_sellp), vp, vp]),
     "lbk_spmv_sellp_f32": (st, [vp, P(lbk_sellp), vp, vp]),
     "lbk_spmv_sellp_adv_f64": (st, [vp, f64, P(lbk_sellp), vp, f64, vp]),
+    "lbk_spmv_sellp_adv_f32": (st, [vp, f32, P(lbk_sellp), vp, f32, vp]),
     "lbk_csr_plan_size": (st, [P(lbk_csr), P(i32)]),
     "lbk_csr_plan": (st, [vp, P(lbk_csr), vp]),
     "lbk_coo_plan_size": (st, [P(lbk_coo), P(i32)]),

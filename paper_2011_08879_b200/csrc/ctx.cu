@@ -244,6 +244,16 @@ lbk_status lbk_memcpy_d2h(lbk_ctx ctx, void* dst, const void* src, size_t bytes)
     });
 }
 
+lbk_status lbk_memcpy_peer(lbk_ctx ctx, void* dst, int dst_device, const void* src,
+                           int src_device, size_t bytes)
+{
+    if (!ctx) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        if (bytes)
+            LBK_CUDA(cudaMemcpyPeerAsync(dst, dst_device, src, src_device, bytes, ctx->stream));
+    });
+}
+
 lbk_status lbk_memcpy_d2d(lbk_ctx ctx, void* dst, const void* src, size_t bytes)
 {
     if (!ctx) return LBK_USAGE_ERROR;

@@ -174,12 +174,15 @@ LBK_SPMV_ADV_ENTRY(lbk_spmv_csr_adv_f32, lbk_csr, run_csr, float, LBK_F32)
 LBK_SPMV_ENTRY(lbk_spmv_coo_f64, lbk_coo, run_coo, double, LBK_F64)
 LBK_SPMV_ENTRY(lbk_spmv_coo_f32, lbk_coo, run_coo, float, LBK_F32)
 LBK_SPMV_ADV_ENTRY(lbk_spmv_coo_adv_f64, lbk_coo, run_coo, double, LBK_F64)
+LBK_SPMV_ADV_ENTRY(lbk_spmv_coo_adv_f32, lbk_coo, run_coo, float, LBK_F32)
 LBK_SPMV_ENTRY(lbk_spmv_ell_f64, lbk_ell, run_ell, double, LBK_F64)
 LBK_SPMV_ENTRY(lbk_spmv_ell_f32, lbk_ell, run_ell, float, LBK_F32)
 LBK_SPMV_ADV_ENTRY(lbk_spmv_ell_adv_f64, lbk_ell, run_ell, double, LBK_F64)
+LBK_SPMV_ADV_ENTRY(lbk_spmv_ell_adv_f32, lbk_ell, run_ell, float, LBK_F32)
 LBK_SPMV_ENTRY(lbk_spmv_sellp_f64, lbk_sellp, run_sellp, double, LBK_F64)
 LBK_SPMV_ENTRY(lbk_spmv_sellp_f32, lbk_sellp, run_sellp, float, LBK_F32)
 LBK_SPMV_ADV_ENTRY(lbk_spmv_sellp_adv_f64, lbk_sellp, run_sellp, double, LBK_F64)
+LBK_SPMV_ADV_ENTRY(lbk_spmv_sellp_adv_f32, lbk_sellp, run_sellp, float, LBK_F32)
 
 lbk_status lbk_csr_plan_size(const lbk_csr* A, int32_t* ntiles_out)
 {

@@ -561,11 +561,11 @@ _SPMV = {
     (CsrMatrix, torch.float64): ("lbk_spmv_csr_f64", "lbk_spmv_csr_adv_f64"),
     (CsrMatrix, torch.float32): ("lbk_spmv_csr_f32", "lbk_spmv_csr_adv_f32"),
     (CooMatrix, torch.float64): ("lbk_spmv_coo_f64", "lbk_spmv_coo_adv_f64"),
-    (CooMatrix, torch.float32): ("lbk_spmv_coo_f32", None),
+    (CooMatrix, torch.float32): ("lbk_spmv_coo_f32", "lbk_spmv_coo_adv_f32"),
     (EllMatrix, torch.float64): ("lbk_spmv_ell_f64", "lbk_spmv_ell_adv_f64"),
-    (EllMatrix, torch.float32): ("lbk_spmv_ell_f32", None),
+    (EllMatrix, torch.float32): ("lbk_spmv_ell_f32", "lbk_spmv_ell_adv_f32"),
     (SellpMatrix, torch.float64): ("lbk_spmv_sellp_f64", "lbk_spmv_sellp_adv_f64"),
-    (SellpMatrix, torch.float32): ("lbk_spmv_sellp_f32", None),
+    (SellpMatrix, torch.float32): ("lbk_spmv_sellp_f32", "lbk_spmv_sellp_adv_f32"),
 }
 
 
