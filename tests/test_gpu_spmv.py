@@ -217,6 +217,17 @@ def test_advanced_apply(O, ex, lk):
             y = lk.vector_from(ex, y0)
             lk.spmv(F, x, y, alpha=alpha, beta=beta)
             assert relerr(lk.vector_to_host(y), exp) <= 1e-14, (name, alpha, beta)
+    # FP32 advanced apply in every format
+    import torch
+    A32 = A.astype(torch.float32)
+    x32, y32 = xh.astype(np.float32), y0.astype(np.float32)
+    ax32 = O.spmv_csr(O.Csr(R.nrows, R.ncols, R.row_ptr, R.cols, R.vals.astype(np.float32)), x32)
+    exp32 = np.float32(2.5) * ax32 + np.float32(-0.5) * y32
+    for name, F in [("csr", A32), ("coo", lk.csr_to_coo(A32)), ("ell", lk.csr_to_ell(A32)),
+                    ("sellp", lk.csr_to_sellp(A32, 32))]:
+        xv, yv = lk.vector_from(ex, x32), lk.vector_from(ex, y32)
+        lk.spmv(F, xv, yv, alpha=2.5, beta=-0.5)
+        assert relerr(lk.vector_to_host(yv), exp32) <= 1e-6, name
     # beta == 0 must not read y (NaN in y stays out)
     x = lk.vector_from(ex, xh)
     y = lk.make_vector(ex, R.nrows)
