@@ -533,14 +533,33 @@ def run_cg(ex, world: int, rank: int, local_rank: int, force_dist: bool = False)
     del A4, ones, b
     torch.cuda.empty_cache()
     rp = (rp - k0).astype(np.int32)
-    m = D.DistMap(n, world, rank, rp, cols)
+    def all_ok(ok: bool, what: str) -> None:
+        # a rank that failed must not leave its peers blocked in a collective
+        if world > 1:
+            f = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(f, op=dist.ReduceOp.MIN)
+            ok = bool(f.item())
+        if not ok:
+            raise RuntimeError(f"distributed CG: {what} failed on some rank")
+
+    m = None
+    try:
+        m = D.DistMap(n, world, rank, rp, cols)
+    except Exception:
+        pass
+    all_ok(m is not None, "partition maps")
     if world > 1:
         D.exchange_requests(m)
         comm = D.Communicator.nccl(local_rank)
     else:  # --cg-dist at N = 1: the same path on a one-rank NCCL communicator
         D.exchange_requests_local([m])
         comm = D.Communicator.nccl_single(local_rank)
-    M = D.DistCsrMatrix(ex, m, rp, vals, nnz)
+    M = None
+    try:
+        M = D.DistCsrMatrix(ex, m, rp, vals, nnz)
+    except Exception:
+        pass
+    all_ok(M is not None, "device matrix")
     cg["mode"] = (f"row-partitioned over {world} GPUs: NCCL halo exchange overlapped with the "
                   f"interior rows, ncclAllReduce per reduction (strong scaling)")
     cg["n_ghost_rank0"] = M.n_ghost
