@@ -309,3 +309,57 @@ def test_paper_fixed_10000_protocol(R, ex, lk, kind):
     # the converged prefix agrees; past convergence the runs are rounding noise
     k = next(i for i, h in enumerate(rr.history) if h <= 1e-8)
     assert abs(next(i for i, h in enumerate(r.residual_history) if h <= 1e-8) - k) <= 1
+
+
+def _g45():
+    p = os.path.join(os.path.dirname(__file__), "golden", "cfg45.npz")
+    if not os.path.exists(p):
+        pytest.skip("tests/golden/cfg45.npz not generated")
+    return np.load(p)
+
+
+def test_cfg4_full_history_vs_reference():
+    """SURVEY.md §8c recommended cfg4 report: iterations 581 +- 1, every
+    residual_history entry within 1e-7 relative of the reference's (~17x the
+    reference's own executor spread), final true residual <= 1e-8, flops."""
+    import torch
+    from paper_2011_08879_b200 import gen, larch as lk
+    g = _g45()
+    ex = lk.CudaExecutor(0)
+    A = gen.stencil(ex, "7pt", 256)
+    b = lk.make_vector(ex, A.nrows)
+    lk.spmv(A, lk.vector_from(ex, np.ones(A.ncols)), b)
+    x = lk.zeros(ex, A.nrows)
+    r = lk.solve(A, b, x, lk.SolverConfig(kind="cg", rel_tol=1e-8, max_iters=20000))
+    assert int(g["cg_iters"]) == 581 and abs(r.iterations - 581) <= 1
+    h, hr = np.array(r.residual_history), g["cg_hist"]
+    k = min(len(h), len(hr))
+    assert np.max(np.abs(h[:k] - hr[:k]) / hr[:k]) <= 1e-7
+    assert r.final_rel_residual <= 1e-8
+    if r.iterations == int(g["cg_iters"]):
+        assert r.flop_count == int(g["cg_flops"])
+
+
+def test_cfg5_report_vs_reference():
+    """SURVEY.md §8c recommended cfg5 report: (1) iterations inside the
+    oracle band (reference 495 / parallel 498, +-3), (2) exact match of the
+    first crossing of tol 1e-6 (275 on both oracle executors), (3) history
+    within 1e-6 relative over the first 40 iterations, (4) final true
+    residual <= tol."""
+    from paper_2011_08879_b200 import gen, larch as lk
+    g = _g45()
+    ex = lk.CudaExecutor(0)
+    A = gen.stencil(ex, "7pt", 256, 0.5)
+    xs = lk.vector_from(ex, gen.seeded_values(A.ncols, 11))
+    b = lk.make_vector(ex, A.nrows)
+    lk.spmv(A, xs, b)
+    x = lk.zeros(ex, A.nrows)
+    r = lk.solve(A, b, x, lk.SolverConfig(kind="bicgstab", rel_tol=1e-8, max_iters=20000))
+    ref_iters = int(g["bicg_iters"])
+    assert ref_iters == 495
+    assert abs(r.iterations - ref_iters) <= 3
+    h, hr = np.array(r.residual_history), g["bicg_hist"]
+    first = lambda hh, tol: int(np.argmax(hh <= tol))  # noqa: E731
+    assert first(h, 1e-6) == first(hr, 1e-6) == 275
+    assert np.max(np.abs(h[:40] - hr[:40]) / hr[:40]) <= 1e-6
+    assert r.final_rel_residual <= 1e-8

@@ -246,3 +246,21 @@ def test_partition_maps_bruteforce(O):
                            (e - b) + np.searchsorted(ghosts, cols))
             assert np.array_equal(loc, exp)
         assert owned == n
+
+
+def test_full_size_goldens_committed():
+    """tests/golden/cfg45.npz (reference library, sequential executor, full
+    size) carries the survey's goldens: CG cfg4 581 iterations, final
+    9.589270e-09, flop KAT; BiCGSTAB cfg5 495 iterations."""
+    p = os.path.join(os.path.dirname(__file__), "golden", "cfg45.npz")
+    if not os.path.exists(p):
+        pytest.skip("cfg45.npz not generated")
+    g = np.load(p)
+    assert int(g["cg_iters"]) == 581 and len(g["cg_hist"]) == 582
+    assert abs(g["cg_hist"][-1] - 9.589270e-09) <= 1e-14
+    assert abs(g["cg_hist"][1] - 5.037289e-01) <= 1e-6
+    n, nnz = 256 ** 3, 117_047_296
+    assert int(g["cg_flops"]) == 581 * (4 * nnz + 16 * n) + 2 * nnz + 4 * n == 428_280_119_296
+    assert int(g["bicg_iters"]) == 495
+    assert abs(g["bicg_hist"][1] - 1.136784e-01) <= 1e-6
+    assert int(g["bicg_flops"]) == 495 * (6 * nnz + 28 * n) + 2 * nnz + 2 * n
