@@ -522,6 +522,13 @@ def run_cg(ex, world: int, rank: int, local_rank: int, force_dist: bool = False)
                                "iters_per_s": r.iterations / r.elapsed,
                                "flop_count": r.flop_count,
                                "gflops_ref_model": r.flop_count / r.elapsed / 1e9}
+        xs = lk.zeros(ex, n)
+        r = lk.solve(A5, b5, xs, lk.SolverConfig(kind="cgs", rel_tol=1e-8, max_iters=20000))
+        cg["cgs_cfg5"] = {"config": "cfg5 matrix and rhs, CGS (krylov.cpp:233-297), tol 1e-8",
+                          "iterations": r.iterations, "final_rel_residual": r.final_rel_residual,
+                          "seconds": r.elapsed, "iters_per_s": r.iterations / r.elapsed,
+                          "flop_count": r.flop_count,
+                          "gflops_ref_model": r.flop_count / r.elapsed / 1e9}
         return cg
     # distributed: this rank's rows of the same matrix
     lo, hi = D.part_range(n, world, rank)
