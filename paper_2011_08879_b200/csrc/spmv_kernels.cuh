@@ -24,8 +24,6 @@
 
 namespace lbk {
 
-constexpr int kLongRow = 32;
-
 template <typename T>
 struct CsrView {
     int nrows, ncols;
@@ -108,28 +106,28 @@ __global__ void coo_plan_kernel(const int* __restrict__ rows, long long nnz, int
                                 long long tile_nnz, int* __restrict__ tile_starts);
 
 // ------------------------------------------------ CSR / COO stream kernels
-// Warp-pipelined, TMA-staged CSR over nnz-balanced, row-aligned tiles (a
-// merge-path split constrained to row boundaries; a giant row gets a wide
-// tile of its own).  Every warp of a persistent grid owns whole tiles and
-// runs its own two-slot pipeline in shared memory:
-//   * lane 0 issues two 1-D bulk copies (cp.async.bulk, L2 evict-first) of
-//     the NEXT tile's vals / col_idx into the free slot, completing on that
-//     slot's mbarrier -- the matrix streams never touch the LSU/L1 data
-//     path (ncu showed the L1 data pipe, not HBM, bounding an LSU-streamed
-//     version at 82% busy);
-//   * meanwhile the warp processes the CURRENT tile lane-per-row: lane l
-//     owns row rb + l (+32 ...), reads its entries from shared memory and
-//     gathers x -- across the warp those gathers hit consecutive rows'
-//     j-th columns, so on banded/stencil matrices they coalesce like ELL;
-//     up to kChunk gathers per lane are in flight before the sum;
-//   * each row is summed sequentially from 0.0 in ascending k with
-//     individually rounded products (no FMA) -- the reference's order
-//     (reference.cpp:82-88), so rows of length <= kLongRow are
-//     BIT-IDENTICAL to the FMA-free reference; longer staged rows are
-//     reduced by the warp (normwise tolerance).
-// Tiles wider than a slot go straight from global memory, warp per row.
-// The tile size is chosen per matrix (~32 rows of mean length, so one pass
-// of the warp covers the tile): see stream_tile_nnz().
+// Warp-pipelined, TMA-staged CSR / COO over nnz-balanced, row-aligned tiles
+// (a merge-path split constrained to row boundaries).  Every warp of a
+// persistent grid owns whole tiles and runs its own slot pipeline in
+// shared memory (warp_tile_loop):
+//   * lane 0 issues 1-D bulk copies (cp.async.bulk, L2 evict-first) of a
+//     later tile's vals / col_idx (/ row_idx) into a free slot, completing
+//     on that slot's mbarrier -- the matrix streams never touch the LSU/L1
+//     data path (ncu showed the L1 data pipe, not HBM, bounding an
+//     LSU-streamed version at 82% busy);
+//   * meanwhile the warp sweeps the current tile (staged_rows): lane-per-row
+//     register gathers for short rows (coalesced like ELL on banded
+//     matrices), entry-parallel in-place products when a pass holds long
+//     rows;
+//   * each row of <= kSeqRow entries is summed sequentially from 0.0 in
+//     ascending k with individually rounded products (no FMA) -- the
+//     reference's order (reference.cpp:82-88), hence BIT-IDENTICAL to the
+//     FMA-free reference; longer rows are reduced by the warp (normwise
+//     tolerance);
+//   * the one row of a tile that can overflow a slot goes from global memory
+//     (warp_row_global), the rest of that tile is staged.
+// The tile size is chosen per matrix (one warp pass of 32*G rows of mean
+// length): see stream_tile_nnz().
 #ifndef LBK_CSR_CAP
 #define LBK_CSR_CAP 1024
 #endif
