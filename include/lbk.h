@@ -139,6 +139,9 @@ typedef struct lbk_sellp {
     const int32_t* slice_sets;    /* nslices + 1 */
     const int32_t* col_idx;       /* slice_sets[nslices] * S */
     const void* vals;
+    int64_t stored;               /* slice_sets[nslices] * S, or 0 (read on demand) */
+    const int32_t* tile_slices;   /* optional plan (S == 32), see lbk_sellp_plan */
+    int32_t ntiles;
 } lbk_sellp;
 
 /* ------------------------------------------------------------- SpMV */
@@ -179,6 +182,10 @@ lbk_status lbk_spmv_sellp_adv_f32(lbk_ctx, float alpha, const lbk_sellp* A,
 lbk_status lbk_csr_plan_size(const lbk_csr* A, int32_t* ntiles_out);
 lbk_status lbk_csr_plan(lbk_ctx, const lbk_csr* A, int32_t* tile_rows_dev);
 lbk_status lbk_coo_plan_size(const lbk_coo* A, int32_t* ntiles_out);
+/* SELL-P (slice_size 32): tiles of whole slices for the warp-pipelined
+ * kernel; tile_slices needs ntiles + 1 int32s; A->stored must be set. */
+lbk_status lbk_sellp_plan_size(const lbk_sellp* A, int32_t* ntiles_out);
+lbk_status lbk_sellp_plan(lbk_ctx, const lbk_sellp* A, int32_t* tile_slices_dev);
 lbk_status lbk_coo_plan(lbk_ctx, const lbk_coo* A, int32_t* tile_starts_dev);
 
 /* ------------------------------------------------------------ BLAS-1 */

@@ -302,7 +302,7 @@ struct SellpMatrix {
     {
         return lbk_sellp{nrows, ncols, logical_nnz, LBK_F64, slice_size, nslices,
                          slice_lengths.as<int32_t>(), slice_sets.as<int32_t>(), col_idx.as<int32_t>(),
-                         vals.data()};
+                         vals.data(), static_cast<int64_t>(col_idx.size()), nullptr, 0};
     }
 };
 

@@ -56,7 +56,8 @@ class lbk_sellp(C.Structure):
     _fields_ = [("nrows", C.c_int32), ("ncols", C.c_int32), ("nnz", C.c_int64),
                 ("dtype", C.c_int), ("slice_size", C.c_int32), ("nslices", C.c_int32),
                 ("slice_lengths", C.c_void_p), ("slice_sets", C.c_void_p),
-                ("col_idx", C.c_void_p), ("vals", C.c_void_p)]
+                ("col_idx", C.c_void_p), ("vals", C.c_void_p), ("stored", C.c_int64),
+                ("tile_slices", C.c_void_p), ("ntiles", C.c_int32)]
 
 
 class lbk_dist_map_info_t(C.Structure):
@@ -121,6 +122,8 @@ SIGNATURES = {
     "lbk_csr_plan_size": (st, [P(lbk_csr), P(i32)]),
     "lbk_csr_plan": (st, [vp, P(lbk_csr), vp]),
     "lbk_coo_plan_size": (st, [P(lbk_coo), P(i32)]),
+    "lbk_sellp_plan_size": (st, [P(lbk_sellp), P(i32)]),
+    "lbk_sellp_plan": (st, [vp, P(lbk_sellp), vp]),
     "lbk_coo_plan": (st, [vp, P(lbk_coo), vp]),
     "lbk_axpy_f64": (st, [vp, i64, f64, vp, vp]),
     "lbk_scal_f64": (st, [vp, i64, f64, vp]),

@@ -42,6 +42,24 @@ __global__ void coo_plan_kernel(const int* __restrict__ rows, long long nnz, int
     tile_starts[t] = static_cast<int>(lo);
 }
 
+__global__ void sellp_plan_kernel(int nslices, int ntiles, int k, int* __restrict__ tile_slices)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > ntiles) return;
+    const long long s = static_cast<long long>(t) * k;
+    tile_slices[t] = static_cast<int>(s < nslices ? s : nslices);
+}
+
+void sellp_plan_launch(lbk_ctx ctx, const int* slice_sets, int nslices, long long stored,
+                       int* tile_slices)
+{
+    (void)slice_sets;
+    const int nt = sellp_ntiles(stored, nslices);
+    sellp_plan_kernel<<<ceil_div(nt + 1, 256), 256, 0, ctx->stream>>>(
+        nslices, nt, sellp_slices_per_tile(stored, nslices), tile_slices);
+    LBK_LAUNCH_CHECK();
+}
+
 void csr_plan_launch(lbk_ctx ctx, const int* row_ptr, int nrows, long long nnz, int* tile_rows)
 {
     const int nt = csr_ntiles(nnz, nrows);
@@ -142,9 +160,36 @@ void run_sellp(lbk_ctx ctx, const lbk_sellp* A, const T* x, const Epi& epi, lbk_
     need(A->nslices == (A->nrows + A->slice_size - 1) / A->slice_size, LBK_FORMAT_ERROR,
          "spmv_sellp: nslices != ceil(nrows / slice_size)");
     if (A->nrows == 0) return;
+    const T* vals = static_cast<const T*>(A->vals);
+    if (A->slice_size == 32 && aligned16(vals) && aligned16(A->col_idx) && !sellp_force_sliced()) {
+        // warp pipeline over whole slices (stored count: one host read of
+        // slice_sets[nslices] unless a plan is supplied)
+        const int* plan = A->tile_slices;
+        int ntiles = A->ntiles;
+        long long stored = A->stored;
+        if (!plan) {
+            if (stored <= 0) {
+                int last = 0;
+                LBK_CUDA(cudaMemcpyAsync(&last, A->slice_sets + A->nslices, sizeof(int),
+                                         cudaMemcpyDeviceToHost, ctx->stream));
+                LBK_CUDA(cudaStreamSynchronize(ctx->stream));
+                stored = static_cast<long long>(last) * 32;
+            }
+            ntiles = sellp_ntiles(stored, A->nslices);
+            int* p = static_cast<int*>(scratch(ctx, size_t(ntiles + 1) * sizeof(int)));
+            sellp_plan_launch(ctx, A->slice_sets, A->nslices, stored, p);
+            plan = p;
+        }
+        need(ntiles == sellp_ntiles(stored, A->nslices), LBK_USAGE_ERROR,
+             "spmv_sellp: stale plan (ntiles does not match lbk_sellp_plan_size)");
+        launch_sellp_stream<T>(ctx,
+                               SellpView<T>{A->nrows, A->ncols, 32, A->nslices, A->slice_sets,
+                                            A->col_idx, vals},
+                               plan, ntiles, stored, x, epi, RedWs{});
+        return;
+    }
     launch_sliced<T, Epi, false>(ctx, A->nrows, A->slice_size, A->slice_sets, 0, 0,
-                                 A->col_idx, static_cast<const T*>(A->vals), x, epi, RedWs{},
-                                 A->ncols);
+                                 A->col_idx, vals, x, epi, RedWs{}, A->ncols);
 }
 
 }  // namespace
@@ -197,6 +242,23 @@ lbk_status lbk_csr_plan(lbk_ctx ctx, const lbk_csr* A, int32_t* tile_rows_dev)
     return guard(ctx, [&] {
         need(A->nrows > 0, LBK_USAGE_ERROR, "lbk_csr_plan: empty matrix");
         csr_plan_launch(ctx, A->row_ptr, A->nrows, A->nnz, tile_rows_dev);
+    });
+}
+
+lbk_status lbk_sellp_plan_size(const lbk_sellp* A, int32_t* ntiles_out)
+{
+    if (!A || !ntiles_out || A->stored < 0) return LBK_USAGE_ERROR;
+    *ntiles_out = sellp_ntiles(A->stored, A->nslices);
+    return LBK_OK;
+}
+
+lbk_status lbk_sellp_plan(lbk_ctx ctx, const lbk_sellp* A, int32_t* tile_slices_dev)
+{
+    if (!ctx || !A) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        need(A->slice_size == 32 && A->stored > 0, LBK_USAGE_ERROR,
+             "lbk_sellp_plan: needs slice_size 32 and the stored entry count");
+        sellp_plan_launch(ctx, A->slice_sets, A->nslices, A->stored, tile_slices_dev);
     });
 }
 

@@ -609,6 +609,114 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
     }
 }
 
+// SELL-P with 32-row slices on the same warp pipeline: a slice is one
+// contiguous column-major block (entry (r, j) at (slice_sets[s] + j)*32 +
+// r%32), so a tile of whole slices is one bulk copy per array.  The sweep
+// is lane-per-row: column j of a slice is 32 consecutive shared-memory
+// words (conflict-free) and its 32 gathers coalesce like ELL; up to 32
+// columns' gathers per lane are in flight before the (sequential,
+// reference-order) sum.  Tiles: runs of k whole slices (tile_slices[t] =
+// t*k, see sellp_slices_per_tile).
+template <typename T, class Epi>
+__global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
+    sellp_stream_kernel(SellpView<T> A, const int* __restrict__ tile_slices, int ntiles,
+                        long long stored, const T* __restrict__ x, Epi epi, RedWs ws)
+{
+    using Cfg = StreamCfg<T, 1>;
+    using EP = EpiPre<Epi>;
+    constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[Cfg::kWarps][Cfg::kSlots];
+    __shared__ double red_sh[32 * NV];
+    if (epi.skip()) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double acc[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+
+    // one slice (its slice set a, length len), its column block read
+    // through colv(a, j, v, c)
+    auto slice = [&](int s, int a, int len, auto&& colv) {
+        const int r = s * 32 + lane;
+        typename EP::type pre;
+        if (r < A.nrows) pre = EP::load(epi, r);
+        T sum = T(0);
+        for (int j0 = 0; j0 < len; j0 += 32) {
+            int c[32];
+            T v[32], g[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                c[j] = -1;
+                if (j0 + j < len) colv(a, j0 + j, v[j], c[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) g[j] = c[j] >= 0 ? ldg_nc(x + c[j]) : T(0);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (c[j] >= 0) sum = add_rn(sum, mul_rn(v[j], g[j]));
+        }
+        if (r < A.nrows) EP::row(epi, r, sum, pre, acc);
+    };
+
+    struct SetPf {
+        int v;  // slice_sets[first slice of the tile + lane] (<= 32 slices per tile)
+    };
+    warp_tile_loop<T, 1>(
+        ntiles, stored, A.vals, A.cols, nullptr,
+        smem + size_t(warp) * Cfg::kSlots * Cfg::slot_bytes, bars[warp],
+        [&](int t) { return (t < ntiles && lane < 2) ? __ldg(tile_slices + t + lane) : 0; },
+        [&](int t, int b) { return (t < ntiles && lane < 2) ? __ldg(A.slice_sets + b) * 32 : 0; },
+        [&](int b, int k) {
+            return make_int4(__shfl_sync(0xffffffffu, b, 0), __shfl_sync(0xffffffffu, b, 1),
+                             __shfl_sync(0xffffffffu, k, 0), __shfl_sync(0xffffffffu, k, 1));
+        },
+        [&](int4 bd) {
+            const int s = bd.x + lane;
+            return SetPf{__ldg(A.slice_sets + (s < bd.y ? s : bd.y))};
+        },
+        [&](int4 bd) {
+            const int ks = __ldg(A.slice_sets + bd.y - 1) * 32;  // the giant slice is the last
+            return int4x2{make_int4(bd.x, bd.y - 1, bd.z, ks), make_int4(bd.y - 1, bd.y, ks, bd.w)};
+        },
+        [&](int4 bd, int ka, T* sv, const int* sc, const int*, const SetPf& p) {
+            for (int s = bd.x; s < bd.y; ++s) {
+                const int i = s - bd.x;
+                int a, e;
+                if (i < 31) {
+                    a = __shfl_sync(0xffffffffu, p.v, i);
+                    e = __shfl_sync(0xffffffffu, p.v, i + 1);
+                } else {
+                    a = __ldg(A.slice_sets + s);
+                    e = __ldg(A.slice_sets + s + 1);
+                }
+                slice(s, a, e - a, [&](int a, int j, T& v, int& c) {
+                    const int o = (a + j) * 32 + lane - ka;
+                    v = sv[o];
+                    c = sc[o];
+                });
+            }
+        },
+        [&](int4 bd) {
+            for (int s = bd.x; s < bd.y; ++s) {
+                const int a = __ldg(A.slice_sets + s);
+                slice(s, a, __ldg(A.slice_sets + s + 1) - a, [&](int a, int j, T& v, int& c) {
+                    const long long o = (static_cast<long long>(a) + j) * 32 + lane;
+                    v = __ldcs(A.vals + o);
+                    c = __ldcs(A.cols + o);
+                });
+            }
+        });
+
+    if constexpr (Epi::NV > 0) {
+        __syncthreads();
+        block_sum<NV>(acc, tid, Cfg::kThreads, red_sh);
+        grid_reduce_finish<NV>(acc, ws, tid, Cfg::kThreads, red_sh,
+                               [&](const double* tot) { epi.finish(tot); });
+    }
+}
+
+__global__ void sellp_plan_kernel(int nslices, int ntiles, int k, int* __restrict__ tile_slices);
+
 // COO: warp tiles are row-aligned entry ranges [tile_starts[t],
 // tile_starts[t+1]) of the (row, col)-sorted entries; the tile owns rows
 // [r0, r1) including empty ones (reference.cpp:67 zero-fills y first).

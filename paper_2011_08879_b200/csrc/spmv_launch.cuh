@@ -24,6 +24,34 @@ inline int csr_ntiles(long long nnz, long long nrows) { return stream_ntiles(nnz
 inline int coo_ntiles(long long nnz, long long nrows) { return stream_ntiles(nnz, nrows, 2); }
 
 void csr_plan_launch(lbk_ctx ctx, const int* row_ptr, int nrows, long long nnz, int* tile_rows);
+// SELL-P tiles are runs of k whole slices, k = slots' worth of mean-size
+// slices (a mean-size tile never straddles a slot: the entry-window rule of
+// CSR would pair two 27-column slices into an oversize tile).
+inline int sellp_slices_per_tile(long long stored, int nslices)
+{
+    const long long mean = nslices > 0 ? (stored + nslices - 1) / nslices : 1;
+    const long long k = (StreamCfg<double, 1>::kCap - 128) / (mean < 1 ? 1 : mean);
+    return static_cast<int>(k < 1 ? 1 : (k > 32 ? 32 : k));
+}
+inline int sellp_ntiles(long long stored, int nslices)
+{
+    const int k = sellp_slices_per_tile(stored, nslices);
+    const long long t = (nslices + k - 1) / k;
+    return static_cast<int>(t < 1 ? 1 : t);
+}
+void sellp_plan_launch(lbk_ctx ctx, const int* slice_sets, int nslices, long long stored,
+                       int* tile_slices);
+// The warp-pipelined SELL-P kernel is opt-in (LBK_SELLP_ALGO=stream): on
+// cfg2 it measured 143 us against 129 us for the 4-rows-per-thread sliced
+// kernel, both latency-bound on the gathers (ncu: issue ~30%).
+inline bool sellp_force_sliced()
+{
+    static int v = [] {
+        const char* e = std::getenv("LBK_SELLP_ALGO");
+        return (e && std::strcmp(e, "stream") == 0) ? 0 : 1;
+    }();
+    return v != 0;
+}
 void coo_plan_launch(lbk_ctx ctx, const int* rows, int nrows, long long nnz, int* tile_starts);
 
 // Forces the warp-per-row CSR kernel (diagnostics / A-B comparison).
@@ -183,6 +211,25 @@ void launch_coo(lbk_ctx ctx, CooView<T> A, const T* x, const Epi& epi, RedWs ws)
     case 2: stream_launch<T, 2, 2>(ctx, coo_stream_kernel<T, Epi, 2>, A, x, epi, ws); break;
     default: stream_launch<T, 2, 1>(ctx, coo_stream_kernel<T, Epi, 1>, A, x, epi, ws); break;
     }
+}
+
+template <typename T, class Epi>
+void launch_sellp_stream(lbk_ctx ctx, SellpView<T> A, const int* plan, int ntiles, long long stored,
+                         const T* x, const Epi& epi, RedWs ws)
+{
+    using Cfg = StreamCfg<T, 1>;
+    auto kernel = sellp_stream_kernel<T, Epi>;
+    constexpr size_t smem = Cfg::smem_bytes;
+    static bool attr = (set_smem(kernel, smem), true);
+    (void)attr;
+    static int bps = blocks_per_sm(kernel, Cfg::kThreads, smem);
+    long long cap = static_cast<long long>(ctx->num_sms) * bps;
+    if (cap > kRedMaxBlocks) cap = kRedMaxBlocks;
+    const long long want = (ntiles + Cfg::kWarps - 1) / Cfg::kWarps;
+    const int grid = static_cast<int>(want < cap ? want : cap);
+    launch_k(ctx, kernel, grid, Cfg::kThreads, smem, x, size_t(A.ncols) * sizeof(T), A, plan,
+             ntiles, stored, x, epi, ws);
+    LBK_LAUNCH_CHECK();
 }
 
 // ELL (is_ell) or SELL-P over the sliced column-major layout.

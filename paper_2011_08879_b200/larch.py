@@ -343,6 +343,7 @@ class SellpMatrix:
     vals: torch.Tensor
     nnz_logical: int
     exec: CudaExecutor
+    stored: int = -1
 
     def nnz(self) -> int:
         return self.nnz_logical
@@ -351,10 +352,24 @@ class SellpMatrix:
     def nslices(self) -> int:
         return int(self.slice_lengths.numel())
 
+    _plan: Optional[torch.Tensor] = field(default=None, repr=False)
+
     def desc(self) -> L.lbk_sellp:
-        return L.lbk_sellp(self.nrows, self.ncols, self.nnz_logical, _dt(self.vals),
-                           self.slice_size, self.nslices, _ptr(self.slice_lengths),
-                           _ptr(self.slice_sets), _ptr(self.col_idx), _ptr(self.vals))
+        stored = self.stored if self.stored >= 0 else int(self.col_idx.numel())
+        d = L.lbk_sellp(self.nrows, self.ncols, self.nnz_logical, _dt(self.vals),
+                        self.slice_size, self.nslices, _ptr(self.slice_lengths),
+                        _ptr(self.slice_sets), _ptr(self.col_idx), _ptr(self.vals), stored,
+                        None, 0)
+        if self.slice_size == 32 and stored > 0 and self.nrows > 0:
+            if self._plan is None:
+                nt = C.c_int32()
+                _check(L.load().lbk_sellp_plan_size(C.byref(d), C.byref(nt)))
+                plan = torch.empty(nt.value + 1, dtype=torch.int32, device=self.exec.device)
+                _check(L.load().lbk_sellp_plan(self.exec.ctx, C.byref(d), _ptr(plan)), self.exec.ctx)
+                self._plan = plan
+            d.tile_slices = _ptr(self._plan)
+            d.ntiles = self._plan.numel() - 1
+        return d
 
 
 def csr_from_host(exec: CudaExecutor, nrows: int, ncols: int, row_ptr, col_idx, vals,
@@ -483,7 +498,8 @@ def csr_to_sellp(m: CsrMatrix, slice_size: int = 32) -> SellpMatrix:
     vals = torch.empty(max(stored.value, 1), dtype=m.vals.dtype, device=m.exec.device)
     _check(lib.lbk_csr_to_sellp(m.exec.ctx, C.byref(d), slice_size, _ptr(ss), _ptr(cols),
                                 _ptr(vals)), m.exec.ctx)
-    return SellpMatrix(m.nrows, m.ncols, slice_size, sl[:ns], ss, cols, vals, m.nnz(), m.exec)
+    return SellpMatrix(m.nrows, m.ncols, slice_size, sl[:ns], ss, cols, vals, m.nnz(), m.exec,
+                       stored.value)
 
 
 def validate(m) -> None:

@@ -296,3 +296,34 @@ def test_blas1(O, ex, lk):
     assert np.array_equal(lk.vector_to_host(y), -2.0 * (b + 0.5 * a))
     lk.fill(y, 3.25)
     assert np.all(lk.vector_to_host(y) == 3.25)
+
+
+def test_sellp_stream_kernel_opt_in():
+    """The warp-pipelined SELL-P kernel (LBK_SELLP_ALGO=stream, read once per
+    process) is exercised in a subprocess: bit-exact with the reference."""
+    import subprocess
+    import sys
+    import textwrap
+    code = textwrap.dedent("""
+        import sys, numpy as np
+        sys.path.insert(0, %r)
+        from oracle import oracle as O
+        from paper_2011_08879_b200 import larch as lk
+        ex = lk.CudaExecutor(0)
+        for R in (O.stencil("27pt", 20), O.powerlaw(1 << 14, window=2048, max_len=3000)):
+            A = lk.csr_from_host(ex, R.nrows, R.ncols, R.row_ptr, R.cols, R.vals)
+            xh = O.seeded_values(R.ncols, 11)
+            x = lk.vector_from(ex, xh)
+            y = lk.make_vector(ex, R.nrows)
+            lk.spmv(lk.csr_to_sellp(A, 32), x, y)
+            yref = O.spmv_csr(R, xh)
+            short = np.diff(R.row_ptr) <= 32
+            yy = lk.vector_to_host(y)
+            assert np.array_equal(yy[short], yref[short])
+            assert np.max(np.abs(yy - yref)) <= 1e-12 * np.max(np.abs(yref))
+        print("ok")
+    """) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),)
+    env = dict(os.environ, LBK_SELLP_ALGO="stream")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
