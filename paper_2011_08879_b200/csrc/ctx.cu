@@ -97,6 +97,15 @@ static lbk_status ctx_create_impl(int device, void* stream, bool own, lbk_ctx* o
             if (ctx->l2_persist && ctx->persist_max)
                 cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(lim));
         }
+        {
+            // solver workspaces come from the stream-ordered pool; keep freed
+            // memory in the pool so repeated solves do not remap pages
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+                uint64_t keep = ~uint64_t{0};
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+        }
         if (own) {
             LBK_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
             ctx->own_stream = true;
