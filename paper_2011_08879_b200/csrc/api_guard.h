@@ -1,6 +1,8 @@
 // api_guard.h -- exception -> lbk_status bridge for every C-ABI entry point.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <string>
 
 #include "lbk_internal.cuh"
@@ -12,6 +14,13 @@ void set_error(lbk_ctx ctx, const std::string& msg);
 // Runs body(); converts lbk::Error / std::bad_alloc / anything else into a
 // status + message.  Mirrors how the reference's CLI maps its exception
 // taxonomy (tools/larch.cpp:375-394), but at the ABI instead of exit codes.
+// NVTX range over a C-ABI call (tracing: nsys / ncu --nvtx attribute
+// device time to the reference-level operation).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 template <typename F>
 lbk_status guard(lbk_ctx ctx, F&& body)
 {

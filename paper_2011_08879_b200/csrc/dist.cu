@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <barrier>
+#include <chrono>
+#include <thread>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -39,6 +41,8 @@ struct NcclApi {
     decltype(&ncclGroupStart) GroupStart = nullptr;
     decltype(&ncclGroupEnd) GroupEnd = nullptr;
     decltype(&ncclGetErrorString) GetErrorString = nullptr;
+    decltype(&ncclCommGetAsyncError) GetAsyncError = nullptr;
+    decltype(&ncclCommAbort) CommAbort = nullptr;
 };
 
 const NcclApi& nccl()
@@ -58,6 +62,9 @@ const NcclApi& nccl()
         a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
         a.GetErrorString =
             reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        a.GetAsyncError =
+            reinterpret_cast<decltype(a.GetAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
+        a.CommAbort = reinterpret_cast<decltype(a.CommAbort)>(dlsym(h, "ncclCommAbort"));
         return a;
     }();
     need(api.GetUniqueId && api.CommInitRank && api.AllReduce && api.Send && api.Recv &&
@@ -102,6 +109,36 @@ struct NcclComm final : Comm {
         LBK_NCCL(N.GroupEnd());
     }
     bool async() const override { return true; }
+    // Poll instead of blocking: a failed peer surfaces as an NCCL async
+    // error (or, past LBK_NCCL_TIMEOUT seconds, default 600, as a timeout);
+    // the communicator is then aborted so the call returns instead of
+    // hanging in the collective.
+    void wait(cudaStream_t s) override
+    {
+        static const double limit = [] {
+            const char* e = std::getenv("LBK_NCCL_TIMEOUT");
+            return e ? std::atof(e) : 600.0;
+        }();
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int spin = 0;; ++spin) {
+            const cudaError_t q = cudaStreamQuery(s);
+            if (q == cudaSuccess) return;
+            if (q != cudaErrorNotReady) LBK_CUDA(q);
+            ncclResult_t ae = ncclSuccess;
+            if (nccl().GetAsyncError) nccl().GetAsyncError(comm, &ae);
+            const double el =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if ((ae != ncclSuccess && ae != ncclInProgress) || el > limit) {
+                if (nccl().CommAbort) nccl().CommAbort(comm);
+                comm = nullptr;
+                fail(LBK_NCCL_ERROR, ae != ncclSuccess
+                                         ? std::string("NCCL async error: ") +
+                                               nccl().GetErrorString(ae)
+                                         : "NCCL wait timed out (LBK_NCCL_TIMEOUT)");
+            }
+            if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+    }
 };
 
 // ------------------------------------------------------------ threads
@@ -508,6 +545,7 @@ lbk_status lbk_dist_csr_destroy(lbk_dist_csr D)
 lbk_status lbk_dist_spmv_f64(lbk_ctx ctx, lbk_dist_csr D, lbk_comm comm, double* x_ext, double* y)
 {
     if (!ctx || !D) return LBK_USAGE_ERROR;
+    NvtxRange nvtx_("lbk_dist_spmv_f64");
     return guard(ctx, [&] {
         need(D->P == 1 || (comm && comm->impl->nranks == D->P && comm->impl->rank == D->rank),
              LBK_USAGE_ERROR, "dist spmv: communicator does not match the partition");

@@ -53,6 +53,9 @@ struct Comm {
     // true if exchange() is asynchronous on s (can overlap compute on
     // another stream)
     virtual bool async() const = 0;
+    // host wait for s; a communicator that can fail asynchronously (NCCL:
+    // a dead peer) polls for that instead of blocking forever
+    virtual void wait(cudaStream_t s) { LBK_CUDA(cudaStreamSynchronize(s)); }
 };
 
 struct DevArr {

@@ -1020,6 +1020,7 @@ struct LocalEnv {
     void apply(const double* x, const Epi& e) { op.apply(ctx, x, e, ws); }
     template <class Op>
     void vec(const Op& o) { launch_vec(ctx, n, o, ws); }
+    void sync() { LBK_CUDA(cudaStreamSynchronize(ctx->stream)); }
     double norm(const double* b)
     {
         double v = 0.0;
@@ -1104,6 +1105,11 @@ struct DistEnv {
         launch_vec(ctx, D->n_local, o, wa);
         finish(o, 1, 0);
     }
+    void sync()
+    {
+        if (comm) comm->wait(ctx->stream);
+        else LBK_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
     double norm(const double* b)
     {
         double* d = ws.out + 24;
@@ -1111,7 +1117,7 @@ struct DistEnv {
         if (reduce()) comm->allreduce_sum(d, 1, ctx->stream);
         double v = 0.0;
         LBK_CUDA(cudaMemcpyAsync(&v, d, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        LBK_CUDA(cudaStreamSynchronize(ctx->stream));
+        sync();
         return std::sqrt(v);
     }
 };
@@ -1165,6 +1171,7 @@ template <class Env>
 void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lbk_solver_cfg* cfg,
                 lbk_solve_result* res, double* history, int hist_cap)
 {
+    NvtxRange nvtx_("lbk_solve");
     // krylov.cpp:449-472 validation
     need(cfg != nullptr && res != nullptr, LBK_USAGE_ERROR, "solve: null config/result");
     need(cfg->max_iters >= 1, LBK_CONFIGURATION_ERROR, "max_iters must be positive");
@@ -1266,7 +1273,7 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
             env.vec(OpGmScale{V, nullptr, st, 0, 0.0});
             LBK_CUDA(cudaMemcpyAsync(done_host, &st->done, sizeof(int), cudaMemcpyDeviceToHost,
                                      ctx->stream));
-            LBK_CUDA(cudaStreamSynchronize(ctx->stream));
+            env.sync();
             if (*done_host) break;
         }
         finish_solve(ctx, env, st, hist, x, x_user, n, limit, cfg, res, history, hist_cap, ev0, ev1);
@@ -1355,7 +1362,7 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
         launched += todo;
         LBK_CUDA(cudaMemcpyAsync(done_host, &st->done, sizeof(int), cudaMemcpyDeviceToHost,
                                  ctx->stream));
-        LBK_CUDA(cudaStreamSynchronize(ctx->stream));
+        env.sync();
         if (*done_host || launched >= limit) break;
     }
     if (gexec) cudaGraphExecDestroy(gexec);

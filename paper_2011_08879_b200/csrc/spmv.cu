@@ -203,12 +203,14 @@ extern "C" {
     lbk_status NAME(lbk_ctx ctx, const DESC* A, const T* x, T* y)                      \
     {                                                                                  \
         if (!ctx) return LBK_USAGE_ERROR;                                              \
+        NvtxRange nvtx_(#NAME);                                                        \
         return guard(ctx, [&] { RUN<T>(ctx, A, x, EpiStore<T>{y}, DT); });             \
     }
 #define LBK_SPMV_ADV_ENTRY(NAME, DESC, RUN, T, DT)                                     \
     lbk_status NAME(lbk_ctx ctx, T alpha, const DESC* A, const T* x, T beta, T* y)     \
     {                                                                                  \
         if (!ctx) return LBK_USAGE_ERROR;                                              \
+        NvtxRange nvtx_(#NAME);                                                        \
         return guard(ctx, [&] { RUN<T>(ctx, A, x, EpiAxpby<T>{y, alpha, beta}, DT); }); \
     }
 
