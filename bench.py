@@ -331,6 +331,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample()
     print(json.dumps(line), flush=True)
+    if args.report_dir:
+        from paper_2011_08879_b200 import report as R
+        os.makedirs(args.report_dir, exist_ok=True)
+        recs = R.records_from_bench(line)
+        for fmt in ("json", "csv", "svg"):
+            with open(os.path.join(args.report_dir, f"bench_records.{fmt}"), "w") as f:
+                f.write(R.emit_report(recs, fmt))
 
 
 def time_launches(ex, call, steps: int, warmup: int) -> float:
@@ -376,7 +383,7 @@ def run_formats(ex, lib, A, x, y, steps: int, warmup: int, no_cfg3: bool) -> dic
         t = time_launches(ex, call, max(steps, 10), max(warmup, 3))
         out[key] = {"us": round(t * 1e6, 2), "gbs": round(nbytes / t / 1e9, 1),
                     "gflops": round(2 * nnz / t / 1e9, 1), "frac": round(nbytes / t / 1e9 / peak, 3),
-                    "bytes": int(nbytes)}
+                    "bytes": int(nbytes), "nnz": int(nnz)}
 
     # in-run bandwidth calibration (BabelStream copy / triad, 2 x 1 GiB + 1 GiB)
     ns = 1 << 27

@@ -153,7 +153,7 @@ def records_from_bench(line: dict) -> List[BenchRecord]:
             continue
         cfg, fmt, prec = key.split("_")
         pid, n, nnz = meta[cfg]
-        nnz = nnz if nnz is not None else int(round(v["gflops"] * 1e9 * v["us"] * 1e-6 / 2))
+        nnz = v.get("nnz") or nnz or int(round(v["gflops"] * 1e9 * v["us"] * 1e-6 / 2))
         t = v["us"] * 1e-6
         base = fmt.rstrip("0123456789")
         r = BenchRecord(f"spmv.{base}.{prec}", "cuda", pid, int(v["bytes"]), 2 * nnz, t,
