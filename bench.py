@@ -234,15 +234,19 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         e2e_step()
     e2e_seq_s = timed(run_seq)
 
-    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    # three non-default streams: work on the legacy default stream would
+    # serialise against the copy streams
+    s_in, s_out, s_mv = (torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev))
     ex_in = lk.CudaExecutor(local_rank, stream=s_in)
     ex_out = lk.CudaExecutor(local_rank, stream=s_out)
+    ex_mv = lk.CudaExecutor(local_rank, stream=s_mv)
     xb = [x.values, torch.empty_like(x.values)]
     yb = [y.values, torch.empty_like(y.values)]
     descs = desc
 
     def run_pipe(e0):
         s_in.wait_event(e0)
+        s_mv.wait_event(e0)
         up_done = [torch.cuda.Event() for _ in range(K)]
         mv_done = [torch.cuda.Event() for _ in range(K)]
         dn_done = [torch.cuda.Event() for _ in range(K)]
@@ -253,14 +257,14 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             lk._check(lib.lbk_memcpy_h2d(ex_in.ctx, C.c_void_p(xb[j].data_ptr()), xhp, 8 * ncols),
                       ex_in.ctx)
             up_done[i].record(s_in)
-            stream.wait_event(up_done[i])
+            s_mv.wait_event(up_done[i])
             if i >= 2:
-                stream.wait_event(dn_done[i - 2])  # y buffer j drained
-            st = lib.lbk_spmv_csr_f64(ctx, C.byref(descs), C.c_void_p(xb[j].data_ptr()),
+                s_mv.wait_event(dn_done[i - 2])  # y buffer j drained
+            st = lib.lbk_spmv_csr_f64(ex_mv.ctx, C.byref(descs), C.c_void_p(xb[j].data_ptr()),
                                       C.c_void_p(yb[j].data_ptr()))
             if st:
-                lk._check(st, ctx)
-            mv_done[i].record(stream)
+                lk._check(st, ex_mv.ctx)
+            mv_done[i].record(s_mv)
             s_out.wait_event(mv_done[i])
             lk._check(lib.lbk_memcpy_d2h(ex_out.ctx, yhp, C.c_void_p(yb[j].data_ptr()), nb),
                       ex_out.ctx)

@@ -81,7 +81,9 @@ lbk_status lbk_ctx_set_l2_persist(lbk_ctx ctx, int on);
 lbk_status lbk_alloc(lbk_ctx ctx, size_t bytes, void** out);
 lbk_status lbk_free(lbk_ctx ctx, void* ptr, size_t bytes);
 /* copy()/array_from_host/array_to_host (device_array.cpp:144-263); device
- * to device across GPUs is a direct peer copy, not 3-hop master staging. */
+ * to device across GPUs is a direct peer copy, not 3-hop master staging.
+ * All copies are stream-ordered on the context's stream (asynchronous with
+ * pinned host memory): lbk_sync before reading a host destination. */
 lbk_status lbk_memcpy_h2d(lbk_ctx ctx, void* dst, const void* src, size_t bytes);
 lbk_status lbk_memcpy_d2h(lbk_ctx ctx, void* dst, const void* src, size_t bytes);
 lbk_status lbk_memcpy_d2d(lbk_ctx ctx, void* dst, const void* src, size_t bytes);

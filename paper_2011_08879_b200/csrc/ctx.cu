@@ -248,8 +248,9 @@ lbk_status lbk_memcpy_d2h(lbk_ctx ctx, void* dst, const void* src, size_t bytes)
 {
     if (!ctx) return LBK_USAGE_ERROR;
     return guard(ctx, [&] {
+        // stream-ordered like every other copy: pinned destinations overlap
+        // with work on other streams; lbk_sync (or an event) before reading
         if (bytes) LBK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-        LBK_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
 
