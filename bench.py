@@ -46,6 +46,8 @@ sys.path.insert(0, ROOT)
 # keep stdout to the one JSON line: NCCL's version banner goes to stdout
 if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
     os.environ["NCCL_DEBUG"] = "WARN"
+# a failed peer must cost minutes, not the driver's whole budget
+os.environ.setdefault("LBK_NCCL_TIMEOUT", "180")
 
 METRIC = "FP64 CSR SpMV GB/s (% of HBM roofline) and CG iters/s at 1/2/4/8 B200"
 WORKLOAD = {"workload": "cfg2: FP64 CSR SpMV, 3D 27-pt Poisson 128^3 (2,097,152 rows, "
@@ -694,7 +696,9 @@ def main() -> None:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        import datetime
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank),
+                                timeout=datetime.timedelta(minutes=5))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
