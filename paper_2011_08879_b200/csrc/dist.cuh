@@ -101,6 +101,10 @@ struct MappedEpi {
     };
     __device__ int local(int r) const { return map ? __ldg(map + r) : r + off; }
     __device__ bool skip() const { return e.skip(); }
+    __device__ void prefetch(int rb, int re) const
+    {
+        if (!map) EpiPf<Epi>::run(e, rb + off, re + off);
+    }
     __device__ Pre pre(int r) const
     {
         const int m = local(r);

@@ -167,6 +167,20 @@ __device__ __forceinline__ void fence_proxy_async_smem()
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// L2 prefetch of one vector's rows [rb, re) by the warp (one 128-B line per
+// lane per step): the epilogue operand streams of a tile are pulled into L2
+// when the tile's matrix data is staged, so the sweep's operand loads hit L2
+// instead of paying a DRAM round trip next to the gathers.
+__device__ __forceinline__ void l2_prefetch_rows(const double* v, int rb, int re)
+{
+    if (!v || re <= rb) return;
+    const char* b = reinterpret_cast<const char*>(v + rb);
+    const char* e = reinterpret_cast<const char*>(v + re);
+    const char* line = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(b) & ~uintptr_t(127));
+    for (const char* p = line + (threadIdx.x & 31) * 128; p < e; p += 32 * 128)
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+
 template <typename T>
 __device__ __forceinline__ T ldg_nc(const T* p)
 {

@@ -120,6 +120,10 @@ struct EpiInit {
         double b;
     };
     __device__ bool skip() const { return false; }
+    __device__ void prefetch(int rb, int re) const
+    {
+        l2_prefetch_rows(b, rb, re);
+    }
     __device__ Pre pre(int i) const { return {b[i]}; }
     __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
     __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
@@ -201,6 +205,12 @@ struct EpiCgK3 {
         double b, p, r;
     };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prefetch(int rb, int re) const
+    {
+        l2_prefetch_rows(b, rb, re);
+        l2_prefetch_rows(p, rb, re);
+        l2_prefetch_rows(r, rb, re);
+    }
     __device__ Pre pre(int i) const { return {b[i], p[i], r[i]}; }
     __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
     __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
@@ -255,6 +265,10 @@ struct EpiTrueRes {
         double b;
     };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0 || !st->verify_pending; }
+    __device__ void prefetch(int rb, int re) const
+    {
+        l2_prefetch_rows(b, rb, re);
+    }
     __device__ Pre pre(int i) const { return {b[i]}; }
     __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
     __device__ void row_pre(int, double s, const Pre& pr, double* acc) const
@@ -299,6 +313,10 @@ struct EpiBiB2 {
         double rt;
     };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prefetch(int rb, int re) const
+    {
+        l2_prefetch_rows(rt, rb, re);
+    }
     __device__ Pre pre(int i) const { return {rt[i]}; }
     __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
     __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
@@ -328,6 +346,10 @@ struct EpiBiB4 {
         double s;
     };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prefetch(int rb, int re) const
+    {
+        l2_prefetch_rows(s, rb, re);
+    }
     __device__ Pre pre(int i) const { return {s[i]}; }
     __device__ void row(int i, double sum, double* acc) const { row_pre(i, sum, pre(i), acc); }
     __device__ void row_pre(int i, double sum, const Pre& pr, double* acc) const
@@ -365,6 +387,13 @@ struct EpiBiB6 {
         double b, p, v, r;
     };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prefetch(int rb, int re) const
+    {
+        l2_prefetch_rows(b, rb, re);
+        l2_prefetch_rows(p, rb, re);
+        l2_prefetch_rows(v, rb, re);
+        l2_prefetch_rows(r, rb, re);
+    }
     __device__ Pre pre(int i) const { return {b[i], p[i], v[i], r[i]}; }
     __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
     __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
@@ -426,6 +455,10 @@ struct EpiCgsV {
         double rt;
     };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prefetch(int rb, int re) const
+    {
+        l2_prefetch_rows(rt, rb, re);
+    }
     __device__ Pre pre(int i) const { return {rt[i]}; }
     __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
     __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
@@ -457,6 +490,13 @@ struct EpiCgsT {
         double x, r, w, rt;
     };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prefetch(int rb, int re) const
+    {
+        l2_prefetch_rows(x, rb, re);
+        l2_prefetch_rows(r, rb, re);
+        l2_prefetch_rows(w, rb, re);
+        l2_prefetch_rows(rt, rb, re);
+    }
     __device__ Pre pre(int i) const { return {x[i], r[i], w[i], rt[i]}; }
     __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
     __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
@@ -484,6 +524,10 @@ struct EpiCgsRes {
         double b;
     };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prefetch(int rb, int re) const
+    {
+        l2_prefetch_rows(b, rb, re);
+    }
     __device__ Pre pre(int i) const { return {b[i]}; }
     __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
     __device__ void row_pre(int, double s, const Pre& pr, double* acc) const
@@ -549,6 +593,10 @@ struct EpiGmRes {
         double b;
     };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prefetch(int rb, int re) const
+    {
+        l2_prefetch_rows(b, rb, re);
+    }
     __device__ Pre pre(int i) const { return {b[i]}; }
     __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
     __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
@@ -624,6 +672,10 @@ struct EpiGmApply {
         double v0;
     };
     __device__ bool skip() const { return gm_step_skip(st, jj); }
+    __device__ void prefetch(int rb, int re) const
+    {
+        l2_prefetch_rows(v0, rb, re);
+    }
     __device__ Pre pre(int i) const { return {v0[i]}; }
     __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
     __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const

@@ -84,6 +84,11 @@ struct EpiAxpby {
         T y;
     };
     __device__ bool skip() const { return false; }
+    __device__ void prefetch(int rb, int re) const
+    {
+        if constexpr (sizeof(T) == 8)
+            if (beta != T(0)) l2_prefetch_rows(reinterpret_cast<const double*>(y), rb, re);
+    }
     __device__ Pre pre(int r) const { return {beta != T(0) ? y[r] : T(0)}; }
     __device__ void row_pre(int r, T s, const Pre& p, double*) const
     {
@@ -261,6 +266,17 @@ struct EpiPre<Epi, std::void_t<typename Epi::Pre>> {
     }
 };
 
+// Epilogues that read DRAM operand vectors declare
+// `void prefetch(int rb, int re) const`; others prefetch nothing.
+template <class Epi, class = void>
+struct EpiPf {
+    __device__ static void run(const Epi&, int, int) {}
+};
+template <class Epi>
+struct EpiPf<Epi, std::void_t<decltype(&Epi::prefetch)>> {
+    __device__ static void run(const Epi& e, int rb, int re) { e.prefetch(rb, re); }
+};
+
 constexpr int kSeqRow = 256;  // staged rows up to this length stay bit-exact
 
 // Phase B of a staged tile.  A lane owns G rows per pass (rows base +
@@ -433,12 +449,12 @@ __device__ __forceinline__ int stage_tile(int k0, int k1, long long nnz4, T* sv,
 // pf(bounds) issues per-lane loads for the first row pass of a tile (CSR:
 // its row_ptr entries) when the tile is staged; staged(...) gets them back.
 template <typename T, int NIDX, class M1, class M2, class Mk, class Pf, class Split, class Staged,
-          class Wide>
+          class Wide, class L2pf>
 __device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const T* vals,
                                                const int* idx0, const int* idx1,
                                                unsigned char* wbase, uint64_t* bar, M1&& meta1,
                                                M2&& meta2, Mk&& mk, Pf&& pf, Split&& split,
-                                               Staged&& staged, Wide&& wide)
+                                               Staged&& staged, Wide&& wide, L2pf&& l2pf)
 {
     using Cfg = StreamCfg<T, NIDX>;
     constexpr int CAP = Cfg::kCap, NW = Cfg::kWarps, NS = Cfg::kSlots;
@@ -496,6 +512,7 @@ __device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const 
                                        idx1, &bar[s], pol);
         }
         q.pf = pf(q.st ? q.bd : make_int4(0, 0, 0, 0));
+        if (q.st) l2pf(q.bd);
         return q;
     };
     // prologue: T_0 .. T_{NS-2} staged, metadata of T_{NS-1} complete and
@@ -599,7 +616,8 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
                 const T s = warp_row_global<T>(ks, ke, A.cols, A.vals, x);
                 if (lane == 0) epi.row(r, s, acc);
             }
-        });
+        },
+        [&](int4 bd) { EpiPf<Epi>::run(epi, bd.x, bd.y); });
 
     if constexpr (Epi::NV > 0) {
         __syncthreads();
@@ -705,7 +723,8 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
                     c = __ldcs(A.cols + o);
                 });
             }
-        });
+        },
+        [&](int4) {});
 
     if constexpr (Epi::NV > 0) {
         __syncthreads();
@@ -786,7 +805,8 @@ __global__ void __launch_bounds__((StreamCfg<T, 2>::kThreads), 2)
                 const T s = warp_row_global<T>(ks, ke, A.cols, A.vals, x);
                 if (lane == 0) epi.row(r, s, acc);
             }
-        });
+        },
+        [&](int4 bd) { EpiPf<Epi>::run(epi, bd.x, bd.y); });
 
     if constexpr (Epi::NV > 0) {
         __syncthreads();
