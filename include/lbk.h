@@ -338,6 +338,28 @@ lbk_status lbk_comm_nccl_unique_id(void* id_out /* 128 bytes */);
 lbk_status lbk_comm_init_nccl(const void* id, int32_t nranks, int32_t rank, int32_t device,
                               lbk_comm* out);
 lbk_status lbk_comm_init_threads(int32_t nranks, lbk_comm* comms_out /* [nranks] */);
+/* Peer-memory group (new; csrc/peer.cuh): every rank maps every peer's
+ * device window, and the halo exchange and the solver's scalar reductions
+ * run as lbk's own kernels storing over NVLink -- no NCCL on the iteration
+ * path, CUDA-graph capturable, reductions summed in rank order (same bits
+ * on every rank).  halo_cap = the largest per-peer ghost count of any rank
+ * (equal on all ranks).  One process per GPU: init, publish the 64-byte
+ * IPC handle over the caller's bootstrap, open all handles (nranks x 64
+ * bytes, in rank order).  In-process: lbk_comm_init_peer_group, one
+ * distinct device per rank (ranks sharing a context could deadlock: a
+ * kernel spinning on a peer's flag blocks device-synchronising calls of
+ * the peer's host thread).  Several ranks on one GPU need one process
+ * each.  At most 16 ranks.  Destroying a peer communicator is collective
+ * (peers may still be storing into its window until they finish). */
+lbk_status lbk_comm_init_peer(int32_t nranks, int32_t rank, int32_t device, int64_t halo_cap,
+                              lbk_comm* out);
+lbk_status lbk_comm_peer_handle(lbk_comm comm, void* handle_out /* 64 bytes */);
+lbk_status lbk_comm_peer_open(lbk_comm comm, const void* handles /* nranks * 64 bytes */);
+lbk_status lbk_comm_init_peer_group(int32_t nranks, const int32_t* devices, int64_t halo_cap,
+                                    lbk_comm* comms_out /* [nranks] */);
+/* Wait for the context's stream and report a communicator failure (NCCL
+ * async error, peer timeout) as LBK_NCCL_ERROR. */
+lbk_status lbk_comm_sync(lbk_ctx ctx, lbk_comm comm);
 lbk_status lbk_comm_destroy(lbk_comm c);
 lbk_status lbk_comm_allreduce_sum_f64(lbk_ctx ctx, lbk_comm comm, double* dev, int32_t count);
 

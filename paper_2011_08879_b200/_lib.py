@@ -157,6 +157,11 @@ SIGNATURES = {
     "lbk_comm_nccl_unique_id": (st, [vp]),
     "lbk_comm_init_nccl": (st, [vp, i32, i32, i32, P(vp)]),
     "lbk_comm_init_threads": (st, [i32, vp]),
+    "lbk_comm_init_peer": (st, [i32, i32, i32, i64, P(vp)]),
+    "lbk_comm_peer_handle": (st, [vp, vp]),
+    "lbk_comm_peer_open": (st, [vp, vp]),
+    "lbk_comm_init_peer_group": (st, [i32, vp, i64, vp]),
+    "lbk_comm_sync": (st, [vp, vp]),
     "lbk_comm_destroy": (st, [vp]),
     "lbk_comm_allreduce_sum_f64": (st, [vp, vp, vp, i32]),
     "lbk_dist_csr_create": (st, [vp, vp, vp, vp, i64, P(vp)]),

@@ -203,6 +203,183 @@ struct ThreadComm final : Comm {
     bool async() const override { return false; }
 };
 
+// ------------------------------------------------ peer-memory group
+// See peer.cuh for the protocol.
+struct PeerComm final : Comm {
+    int device = 0;
+    PeerHdr* local = nullptr;       // this rank's window (owned)
+    std::vector<void*> opened;      // IPC-mapped peer windows (closed on destroy)
+    PeerDev pd{};
+    bool ready = false;
+    int* err_host = nullptr;  // pinned
+    ~PeerComm() override
+    {
+        for (void* p : opened) cudaIpcCloseMemHandle(p);
+        if (local) cudaFree(local);
+        if (err_host) cudaFreeHost(err_host);
+    }
+    const PeerDev* peer() const override
+    {
+        need(ready, LBK_USAGE_ERROR, "peer communicator: peers not opened yet");
+        return &pd;
+    }
+    void allreduce_sum(double* dev, int count, cudaStream_t s) override;
+    void exchange(const double*, const std::vector<int>&, double*, const std::vector<int>&,
+                  cudaStream_t) override
+    {
+        fail(LBK_INTERNAL, "peer communicator: halo runs in the pack/receive kernels");
+    }
+    bool async() const override { return true; }
+    void wait(cudaStream_t s) override
+    {
+        // stream-ordered read of the error word: a legacy-stream copy could
+        // wait on a peer's stream that is itself waiting for this rank
+        LBK_CUDA(cudaMemcpyAsync(err_host, &local->error, sizeof(int), cudaMemcpyDeviceToHost, s));
+        LBK_CUDA(cudaStreamSynchronize(s));
+        if (*err_host == 0) return;
+        long long info[4] = {0, 0, 0, 0};
+        cudaMemcpy(info, local->err_info, sizeof(info), cudaMemcpyDeviceToHost);
+        static const char* what[] = {"halo values", "halo slot hand-back", "reduction totals"};
+        fail(LBK_NCCL_ERROR, "peer communicator: rank " + std::to_string(rank) +
+                                 " timed out waiting for " + what[info[0] % 3] + " of rank " +
+                                 std::to_string(info[1]) + " (epoch " + std::to_string(info[2]) +
+                                 ", seen " + std::to_string(info[3]) +
+                                 "; LBK_PEER_TIMEOUT); the group is unusable");
+    }
+    void create(int P, int r, int dev, long long cap)
+    {
+        need(P >= 1 && P <= kPeerMax, LBK_USAGE_ERROR,
+             "peer communicator: at most " + std::to_string(kPeerMax) + " ranks");
+        need(r >= 0 && r < P && cap >= 0, LBK_USAGE_ERROR, "peer communicator: bad rank/cap");
+        nranks = P;
+        rank = r;
+        device = dev;
+        LBK_CUDA(cudaSetDevice(dev));
+        const size_t bytes = kPeerHdrBytes + size_t(2) * P * size_t(cap) * sizeof(double);
+        LBK_CUDA(cudaMallocHost(&err_host, sizeof(int)));
+        *err_host = 0;
+        LBK_CUDA(cudaMalloc(&local, bytes));
+        LBK_CUDA(cudaMemset(local, 0, bytes));
+        PeerHdr h{};
+        const char* e = std::getenv("LBK_PEER_TIMEOUT");
+        h.timeout_ns = static_cast<long long>((e ? std::atof(e) : 300.0) * 1e9);
+        h.cap = cap;
+        LBK_CUDA(cudaMemcpy(local, &h, sizeof(h), cudaMemcpyHostToDevice));
+        pd.P = P;
+        pd.rank = r;
+        pd.debug = std::getenv("LBK_PEER_DEBUG") ? 1 : 0;
+        pd.cap = cap;
+        pd.win[r] = local;
+    }
+    // every window must use the same slot capacity (senders index the
+    // receiver's staging area with their own cap)
+    void verify_caps() const
+    {
+        for (int q = 0; q < nranks; ++q) {
+            long long c = -1;
+            LBK_CUDA(cudaMemcpy(&c, &pd.win[q]->cap, sizeof(c), cudaMemcpyDefault));
+            need(c == pd.cap, LBK_USAGE_ERROR,
+                 "peer communicator: ranks disagree on the halo capacity");
+        }
+    }
+};
+
+__global__ void peer_allreduce_kernel(PeerDev pd, double* dev, int count)
+{
+    const int lane = threadIdx.x;
+    const double v = lane < count ? dev[lane] : 0.0;
+    const double t = peer_allreduce_warp(pd, v, count);
+    if (lane < count) dev[lane] = t;
+}
+
+void PeerComm::allreduce_sum(double* dev, int count, cudaStream_t s)
+{
+    need(count >= 0 && count <= kPeerRedMax, LBK_USAGE_ERROR,
+         "peer allreduce: at most " + std::to_string(kPeerRedMax) + " values");
+    need(ready, LBK_USAGE_ERROR, "peer communicator: peers not opened yet");
+    peer_allreduce_kernel<<<1, 32, 0, s>>>(pd, dev, count);
+    LBK_LAUNCH_CHECK();
+}
+
+// rank q of the (<= kPeerMax) segments [off[q], off[q+1]) holding entry i
+__device__ __forceinline__ int seg_of(const int* off, int P, int i)
+{
+    int q = 0;
+    while (q + 1 < P && i >= off[q + 1]) ++q;
+    return q;
+}
+
+// gather x[send_idx] and store each peer's run into its staging slot
+// (parity e & 1, source = this rank), then raise the peers' `full` flags
+__global__ void peer_push_kernel(PeerDev pd, const int* __restrict__ send_off,
+                                 const int* __restrict__ send_idx, const double* __restrict__ x)
+{
+    __shared__ int so[kPeerMax + 1];
+    PeerHdr* me = pd.win[pd.rank];
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&me->seq_x) + 1;
+    const int par = static_cast<int>(e & 1);
+    if (threadIdx.x <= pd.P) so[threadIdx.x] = send_off[threadIdx.x];
+    __syncthreads();
+    const int q0 = threadIdx.x;
+    if (q0 < pd.P && so[q0 + 1] > so[q0] && e > 2) peer_wait_ge(&me->empty[q0], e - 2, me, 1, q0);
+    __syncthreads();
+    const int ns = so[pd.P];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) {
+        const int q = seg_of(so, pd.P, i);
+        pd.stage(q, par, pd.rank)[i - so[q]] = x[__ldg(send_idx + i)];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (atomicAdd(&me->push_cnt, 1u) == gridDim.x - 1) {
+            me->push_cnt = 0;
+            __threadfence_system();
+            for (int q = 0; q < pd.P; ++q)
+                if (so[q + 1] > so[q]) st_release_sys(&pd.win[q]->full[pd.rank], e);
+            if (pd.debug) printf("[peer] rank %d push epoch %llu n %d\n", pd.rank, e, ns);
+        }
+    }
+}
+
+// wait for the neighbours' pushes of epoch e, copy the staged ghosts behind
+// x_local, hand the slots back, advance the halo epoch
+__global__ void peer_recv_kernel(PeerDev pd, const int* __restrict__ recv_off,
+                                 double* __restrict__ ghost)
+{
+    __shared__ int ro[kPeerMax + 1];
+    PeerHdr* me = pd.win[pd.rank];
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&me->seq_x) + 1;
+    const int par = static_cast<int>(e & 1);
+    if (threadIdx.x <= pd.P) ro[threadIdx.x] = recv_off[threadIdx.x];
+    __syncthreads();
+    const int q0 = threadIdx.x;
+    if (q0 < pd.P && ro[q0 + 1] > ro[q0]) peer_wait_ge(&me->full[q0], e, me, 0, q0);
+    __syncthreads();
+    const int nr = ro[pd.P];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x) {
+        const int q = seg_of(ro, pd.P, i);
+        ghost[i] = __ldcv(pd.stage(pd.rank, par, q) + (i - ro[q]));
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (atomicAdd(&me->recv_cnt, 1u) == gridDim.x - 1) {
+            me->recv_cnt = 0;
+            __threadfence_system();
+            for (int q = 0; q < pd.P; ++q)
+                if (ro[q + 1] > ro[q]) st_release_sys(&pd.win[q]->empty[pd.rank], e);
+            *reinterpret_cast<volatile unsigned long long*>(&me->seq_x) = e;
+            if (pd.debug) printf("[peer] rank %d recv epoch %llu n %d\n", pd.rank, e, nr);
+        }
+    }
+}
+
+int peer_grid(int n)
+{
+    const int b = ceil_div(n, 256);
+    return b < 1 ? 1 : (b > 296 ? 296 : b);
+}
+
 __global__ void pack_kernel(int n, const int* __restrict__ idx, const double* __restrict__ x,
                             double* __restrict__ out)
 {
@@ -262,6 +439,26 @@ void dist_pack(lbk_ctx ctx, const lbk_dist_csr_s* D, const double* x)
     if (n == 0) return;
     pack_kernel<<<ceil_div(n, 256) < 1184 ? ceil_div(n, 256) : 1184, 256, 0, ctx->stream>>>(
         n, D->send_idx.as<int>(), x, D->send_buf.as<double>());
+    LBK_LAUNCH_CHECK();
+}
+
+void peer_push(lbk_ctx ctx, const lbk_dist_csr_s* D, const PeerDev& pd, const double* x)
+{
+    need(pd.P == D->P && pd.rank == D->rank, LBK_USAGE_ERROR,
+         "dist spmv: communicator does not match the partition");
+    for (int q = 0; q < D->P; ++q)
+        need(D->send_off[q + 1] - D->send_off[q] <= pd.cap &&
+                 D->recv_off[q + 1] - D->recv_off[q] <= pd.cap,
+             LBK_USAGE_ERROR, "peer communicator: halo capacity too small for this matrix");
+    peer_push_kernel<<<peer_grid(D->send_off.back()), 256, 0, ctx->stream>>>(
+        pd, D->send_off_d.as<int>(), D->send_idx.as<int>(), x);
+    LBK_LAUNCH_CHECK();
+}
+
+void peer_recv(lbk_ctx ctx, const lbk_dist_csr_s* D, const PeerDev& pd, double* ghost)
+{
+    peer_recv_kernel<<<peer_grid(D->recv_off.back()), 256, 0, ctx->stream>>>(
+        pd, D->recv_off_d.as<int>(), ghost);
     LBK_LAUNCH_CHECK();
 }
 
@@ -469,6 +666,104 @@ lbk_status lbk_comm_init_threads(int32_t nranks, lbk_comm* comms_out)
     });
 }
 
+lbk_status lbk_comm_init_peer(int32_t nranks, int32_t rank, int32_t device, int64_t halo_cap,
+                              lbk_comm* out)
+{
+    if (!out) return LBK_USAGE_ERROR;
+    return guard(nullptr, [&] {
+        auto c = std::make_unique<PeerComm>();
+        c->create(nranks, rank, device, halo_cap);
+        if (nranks == 1) c->ready = true;
+        auto h = std::make_unique<lbk_comm_s>();
+        h->impl = c.release();
+        *out = h.release();
+    });
+}
+
+lbk_status lbk_comm_peer_handle(lbk_comm comm, void* handle_out)
+{
+    if (!comm || !handle_out) return LBK_USAGE_ERROR;
+    return guard(nullptr, [&] {
+        auto* c = dynamic_cast<PeerComm*>(comm->impl);
+        need(c != nullptr, LBK_USAGE_ERROR, "not a peer communicator");
+        LBK_CUDA(cudaSetDevice(c->device));
+        cudaIpcMemHandle_t h;
+        LBK_CUDA(cudaIpcGetMemHandle(&h, c->local));
+        std::memcpy(handle_out, &h, sizeof(h));
+    });
+}
+
+lbk_status lbk_comm_peer_open(lbk_comm comm, const void* handles)
+{
+    if (!comm || !handles) return LBK_USAGE_ERROR;
+    return guard(nullptr, [&] {
+        auto* c = dynamic_cast<PeerComm*>(comm->impl);
+        need(c != nullptr, LBK_USAGE_ERROR, "not a peer communicator");
+        need(!c->ready || c->nranks == 1, LBK_USAGE_ERROR, "peer communicator already open");
+        LBK_CUDA(cudaSetDevice(c->device));
+        const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+        for (int q = 0; q < c->nranks; ++q) {
+            if (q == c->rank) continue;
+            void* p = nullptr;
+            LBK_CUDA(cudaIpcOpenMemHandle(&p, hs[q], cudaIpcMemLazyEnablePeerAccess));
+            c->opened.push_back(p);
+            c->pd.win[q] = static_cast<PeerHdr*>(p);
+        }
+        c->verify_caps();
+        c->ready = true;
+    });
+}
+
+lbk_status lbk_comm_init_peer_group(int32_t nranks, const int32_t* devices, int64_t halo_cap,
+                                    lbk_comm* comms_out)
+{
+    if (!comms_out || !devices || nranks < 1) return LBK_USAGE_ERROR;
+    return guard(nullptr, [&] {
+        // one context per rank: ranks sharing a device (and so a context)
+        // could deadlock -- a kernel spinning on a peer's flag blocks any
+        // device-synchronising call (cudaFree, lazy module load, ...) the
+        // peer's host thread makes before it posts
+        for (int r = 0; r < nranks; ++r)
+            for (int q = 0; q < r; ++q)
+                need(devices[r] != devices[q], LBK_USAGE_ERROR,
+                     "peer group: one device per rank (use one process per rank to fold "
+                     "several ranks onto one GPU)");
+        std::vector<std::unique_ptr<PeerComm>> cs;
+        for (int r = 0; r < nranks; ++r) {
+            cs.push_back(std::make_unique<PeerComm>());
+            cs.back()->create(nranks, r, devices[r], halo_cap);
+        }
+        for (int r = 0; r < nranks; ++r)
+            for (int q = 0; q < nranks; ++q) {
+                cs[r]->pd.win[q] = cs[q]->local;
+                if (devices[r] != devices[q]) {
+                    int ok = 0;
+                    LBK_CUDA(cudaDeviceCanAccessPeer(&ok, devices[r], devices[q]));
+                    need(ok, LBK_USAGE_ERROR, "peer group: devices without peer access");
+                    LBK_CUDA(cudaSetDevice(devices[r]));
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(devices[q], 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                    else LBK_CUDA(e);
+                }
+            }
+        for (int r = 0; r < nranks; ++r) {
+            cs[r]->ready = true;
+            auto h = std::make_unique<lbk_comm_s>();
+            h->impl = cs[r].release();
+            comms_out[r] = h.release();
+        }
+    });
+}
+
+lbk_status lbk_comm_sync(lbk_ctx ctx, lbk_comm comm)
+{
+    if (!ctx) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        if (comm) comm->impl->wait(ctx->stream);
+        else LBK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 lbk_status lbk_comm_destroy(lbk_comm c)
 {
     if (c) {
@@ -514,6 +809,12 @@ lbk_status lbk_dist_csr_create(lbk_ctx ctx, lbk_dist_map m, const int32_t* row_p
         D->send_buf.alloc(ns * 8);
         if (ns)
             LBK_CUDA(cudaMemcpy(D->send_idx.p, m->send_idx.data(), ns * 4, cudaMemcpyHostToDevice));
+        D->send_off_d.alloc(size_t(D->P + 1) * 4);
+        D->recv_off_d.alloc(size_t(D->P + 1) * 4);
+        LBK_CUDA(cudaMemcpy(D->send_off_d.p, D->send_off.data(), size_t(D->P + 1) * 4,
+                            cudaMemcpyHostToDevice));
+        LBK_CUDA(cudaMemcpy(D->recv_off_d.p, D->recv_off.data(), size_t(D->P + 1) * 4,
+                            cudaMemcpyHostToDevice));
         LBK_CUDA(cudaStreamCreateWithFlags(&D->comm_stream, cudaStreamNonBlocking));
         LBK_CUDA(cudaEventCreateWithFlags(&D->ev_pack, cudaEventDisableTiming));
         LBK_CUDA(cudaEventCreateWithFlags(&D->ev_recv, cudaEventDisableTiming));

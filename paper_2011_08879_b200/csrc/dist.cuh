@@ -22,6 +22,7 @@
 
 #include <vector>
 
+#include "peer.cuh"
 #include "spmv_launch.cuh"
 
 struct lbk_dist_map_s {
@@ -56,6 +57,10 @@ struct Comm {
     // host wait for s; a communicator that can fail asynchronously (NCCL:
     // a dead peer) polls for that instead of blocking forever
     virtual void wait(cudaStream_t s) { LBK_CUDA(cudaStreamSynchronize(s)); }
+    // peer-memory group (peer.cuh): the halo and the scalar reductions run
+    // in lbk's own kernels over the mapped windows instead of exchange() /
+    // allreduce_sum()
+    virtual const PeerDev* peer() const { return nullptr; }
 };
 
 struct DevArr {
@@ -156,6 +161,7 @@ struct lbk_dist_csr_s {
     lbk::SubCsr interior, boundary;
     std::vector<int> send_off, recv_off;
     lbk::DevArr send_idx, send_buf;
+    lbk::DevArr send_off_d, recv_off_d;  // P + 1 each (peer-memory kernels)
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_pack = nullptr, ev_recv = nullptr;
     int device = 0;
@@ -168,6 +174,10 @@ struct lbk_comm_s {
 namespace lbk {
 
 void dist_pack(lbk_ctx ctx, const lbk_dist_csr_s* D, const double* x);
+// peer-memory halo: gather + remote store into the neighbours' staging
+// slots, and (after the interior rows) wait + copy the staged ghosts
+void peer_push(lbk_ctx ctx, const lbk_dist_csr_s* D, const PeerDev& pd, const double* x);
+void peer_recv(lbk_ctx ctx, const lbk_dist_csr_s* D, const PeerDev& pd, double* ghost);
 
 // y = A x_ext with the halo exchange overlapped with the interior rows.
 // `epi` reduces over interior rows into ws_a.out and boundary rows into
@@ -177,6 +187,14 @@ void dist_apply(lbk_ctx ctx, lbk_dist_csr_s* D, Comm* comm, double* x_ext, const
                 RedWs ws_a, RedWs ws_b)
 {
     const bool xchg = comm && comm->nranks > 1;
+    if (xchg && comm->peer()) {
+        const PeerDev& pd = *comm->peer();
+        peer_push(ctx, D, pd, x_ext);
+        if (D->interior.nrows > 0) launch_sub(ctx, D->interior, x_ext, epi, ws_a);
+        peer_recv(ctx, D, pd, x_ext + D->n_local);
+        if (D->boundary.nrows > 0) launch_sub(ctx, D->boundary, x_ext, epi, ws_b);
+        return;
+    }
     if (xchg) {
         dist_pack(ctx, D, x_ext);
         if (comm->async()) {

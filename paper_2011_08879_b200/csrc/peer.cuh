@@ -1,0 +1,143 @@
+// peer.cuh -- the NVLink peer-memory communicator.
+//
+// Each rank owns one device "window" (cudaMalloc, exported as a CUDA IPC
+// handle; in-process groups share the pointer).  Every rank maps every
+// peer's window, so the two collectives of the distributed solver are plain
+// loads and stores over NVLink issued by lbk's own kernels -- no NCCL on
+// the iteration path, no host involvement, and CUDA-graph capturable:
+//
+//   halo     the pack kernel gathers the values a peer needs and stores
+//            them straight into that peer's staging slot, then raises the
+//            peer's `full` flag; after the interior rows, the receive kernel
+//            waits for the flags of its neighbours, copies the staged ghosts
+//            behind x_local and hands the slot back (`empty` flag in the
+//            sender's window).
+//   scalars  the finishing kernel of each fused reduction posts the rank's
+//            totals into every window's `red` slot, waits for all P posts
+//            and sums them in rank order -- the same bits on every rank --
+//            then advances the solver recurrence (combine + allreduce +
+//            finish in one launch).
+//
+// Epochs are device counters (seq_x, seq_r) so captured graphs replay
+// correctly.  Slots are double-buffered by epoch parity: a sender may only
+// reuse a halo slot once the receiver has consumed the epoch before last
+// (`empty`); a reduction slot of parity p is rewritten two epochs later,
+// which every rank can only reach after all ranks have read it.  Waits spin
+// with a timeout (LBK_PEER_TIMEOUT seconds, default 300); a timeout raises
+// the sticky `error` word that the host reports as LBK_NCCL_ERROR.
+#pragma once
+
+#include "lbk_internal.cuh"
+
+namespace lbk {
+
+constexpr int kPeerMax = 16;     // ranks per peer group (one NVSwitch node)
+constexpr int kPeerRedMax = 16;  // values per reduction
+
+struct PeerHdr {
+    unsigned long long full[kPeerMax];   // halo epoch rank q pushed into me
+    unsigned long long empty[kPeerMax];  // halo epoch rank q consumed from me
+    unsigned long long redf[kPeerMax];   // reduction epoch rank q posted to me
+    double red[2][kPeerMax][kPeerRedMax];
+    unsigned long long seq_x, seq_r;     // local epochs (this rank only)
+    unsigned int push_cnt, recv_cnt;     // last-block counters
+    int error;
+    int pad_;
+    long long err_info[4];  // first timeout: {what (0 halo full, 1 halo empty,
+                            // 2 reduction), peer, wanted epoch, seen epoch}
+    long long timeout_ns;
+    long long cap;  // halo values per (parity, source) slot -- equal on all ranks
+};
+
+constexpr size_t kPeerHdrBytes = (sizeof(PeerHdr) + 255) / 256 * 256;
+
+// Kernel argument: every rank's window as mapped into this process.
+struct PeerDev {
+    PeerHdr* win[kPeerMax];
+    int P = 0, rank = 0;
+    long long cap = 0;
+    int debug = 0;  // LBK_PEER_DEBUG: device printf of every epoch
+    // staging slot (parity par, source src) inside rank q's window
+    __device__ double* stage(int q, int par, int src) const
+    {
+        return reinterpret_cast<double*>(reinterpret_cast<char*>(win[q]) + kPeerHdrBytes) +
+               (static_cast<size_t>(par) * P + src) * cap;
+    }
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Spin until *f >= e (acquire), the group fails, or the timeout expires.
+__device__ __forceinline__ void peer_wait_ge(const unsigned long long* f, unsigned long long e,
+                                             PeerHdr* me, int what, int peer)
+{
+    if (ld_acquire_sys(f) >= e) return;
+    const unsigned long long t0 = global_ns();
+    unsigned long long seen;
+    while ((seen = ld_acquire_sys(f)) < e) {
+        if (*reinterpret_cast<volatile int*>(&me->error)) return;
+        if (global_ns() - t0 > static_cast<unsigned long long>(me->timeout_ns)) {
+            if (atomicExch(&me->error, 1) == 0) {
+                me->err_info[0] = what;
+                me->err_info[1] = peer;
+                me->err_info[2] = static_cast<long long>(e);
+                me->err_info[3] = static_cast<long long>(seen);
+            }
+            return;
+        }
+        __nanosleep(100);
+    }
+}
+
+// One warp.  Lane i < n contributes v; returns the rank-ordered sum over
+// all ranks in lane i (identical bits on every rank).
+__device__ __forceinline__ double peer_allreduce_warp(const PeerDev& pd, double v, int n)
+{
+    const int lane = threadIdx.x & 31;
+    PeerHdr* me = pd.win[pd.rank];
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&me->seq_r) + 1;
+    const int par = static_cast<int>(e & 1);
+    if (lane < n)
+        for (int q = 0; q < pd.P; ++q)
+            *reinterpret_cast<volatile double*>(&pd.win[q]->red[par][pd.rank][lane]) = v;
+    __threadfence_system();
+    __syncwarp();
+    if (lane == 0)
+        for (int q = 0; q < pd.P; ++q) st_release_sys(&pd.win[q]->redf[pd.rank], e);
+    // every lane waits for every post (local loads): no rank can run two
+    // epochs ahead of another, which is what makes parity reuse safe
+    for (int q = 0; q < pd.P; ++q) peer_wait_ge(&me->redf[q], e, me, 2, q);
+    double t = 0.0;
+    if (lane < n)
+        for (int q = 0; q < pd.P; ++q)
+            t = add_rn(t, *reinterpret_cast<volatile double*>(&me->red[par][q][lane]));
+    __syncwarp();
+    if (lane == 0) {
+        *reinterpret_cast<volatile unsigned long long*>(&me->seq_r) = e;
+        if (pd.debug)
+            printf("[peer] rank %d reduce epoch %llu n %d sum0 %.17g flags %llu %llu err %d "
+                   "vals %.17g %.17g\n",
+                   pd.rank, e, n, t, ld_acquire_sys(&me->redf[0]),
+                   pd.P > 1 ? ld_acquire_sys(&me->redf[1]) : 0ull, me->error,
+                   *reinterpret_cast<volatile double*>(&me->red[par][0][0]),
+                   pd.P > 1 ? *reinterpret_cast<volatile double*>(&me->red[par][1][0]) : 0.0);
+    }
+    return t;
+}
+
+}  // namespace lbk

@@ -1109,6 +1109,29 @@ __global__ void finish_kernel(E e, const double* tot)
     e.finish(t);
 }
 
+// Peer-memory group: combine + the rank-ordered sum over the peers'
+// windows + finish() in one launch (peer.cuh).
+template <class E>
+__global__ void peer_finish_kernel(E e, const double* base, int has_a, int has_b, PeerDev pd)
+{
+    if (e.skip()) {
+        if (pd.debug && threadIdx.x == 0) printf("[peer] rank %d finish skipped\n", pd.rank);
+        return;
+    }
+    static_assert(E::NV <= 8, "peer finish: at most 8 values");
+    const int lane = threadIdx.x;
+    double v = 0.0;
+    if (lane < E::NV) {
+        if (has_a) v = add_rn(v, base[lane]);
+        if (has_b) v = add_rn(v, base[8 + lane]);
+    }
+    const double t = peer_allreduce_warp(pd, v, E::NV);
+    __shared__ double tot[8];
+    if (lane < E::NV) tot[lane] = t;
+    __syncwarp();
+    if (lane == 0) e.finish(tot);
+}
+
 struct DistEnv {
     lbk_ctx ctx;
     lbk_dist_csr_s* D;
@@ -1119,7 +1142,6 @@ struct DistEnv {
     long long n_global() const { return D->n_global; }
     long long nnz_global() const { return D->nnz_global; }
     bool ext_x() const { return true; }
-    bool multi() const { return comm && comm->nranks > 1; }
     // asynchronous (NCCL) or no communicator: capturable; the thread group
     // synchronises on the host
     bool graph_ok() const
@@ -1134,6 +1156,11 @@ struct DistEnv {
     template <class E>
     void finish(const E& e, int has_a, int has_b)
     {
+        if (const PeerDev* pd = comm ? comm->peer() : nullptr) {
+            peer_finish_kernel<E><<<1, 32, 0, ctx->stream>>>(e, ws.out, has_a, has_b, *pd);
+            LBK_LAUNCH_CHECK();
+            return;
+        }
         combine_kernel<E::NV><<<1, 32, 0, ctx->stream>>>(ws.out, has_a, has_b);
         LBK_LAUNCH_CHECK();
         if (reduce()) comm->allreduce_sum(ws.out + 16, E::NV, ctx->stream);

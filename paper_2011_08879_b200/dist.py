@@ -17,6 +17,13 @@ sub-matrices.
 Communicators:
   * ``Communicator.nccl`` -- one process per GPU (torchrun); the NCCL
     unique id is broadcast by torch.distributed.
+  * ``Communicator.peer`` -- one process per GPU over peer memory: every
+    rank maps every peer's device window (CUDA IPC handles swapped over
+    torch.distributed) and lbk's own kernels store the halo and the
+    solver's scalar totals over NVLink. No NCCL on the iteration path.
+  * ``Communicator.peer_group(devices)`` -- the same in one process, one
+    host thread and one distinct device per rank. Several ranks on one GPU
+    need one process each (a context shared by ranks could deadlock).
   * ``Communicator.threads(P)`` -- P host threads, each driving its own
     executor; P virtual ranks on one GPU, or single-process multi-GPU.
 """
@@ -116,6 +123,14 @@ class DistMap:
         _check(self.lib.lbk_dist_map_set_sends(self.h, _p(off), _p(gids)))
         self.refresh()
 
+    def halo_count(self) -> int:
+        """Largest number of halo values this rank exchanges with one peer
+        (either direction); the peer communicator's slot size is the max of
+        this over all ranks."""
+        _, goff = self.ghosts()
+        soff, _ = self.sends()
+        return int(max(np.max(np.diff(goff), initial=0), np.max(np.diff(soff), initial=0)))
+
     def sends(self) -> tuple[np.ndarray, np.ndarray]:
         off = np.empty(self.nparts + 1, np.int32)
         idx = np.empty(max(self.info.n_send, 0), np.int32)
@@ -138,6 +153,14 @@ def exchange_requests(m: DistMap, group=None) -> None:
     everyone: list = [None] * m.nparts
     dist.all_gather_object(everyone, mine, group=group)
     m.set_sends([np.asarray(everyone[q][m.rank], np.int32) for q in range(m.nparts)])
+
+
+def peer_halo_cap(m: DistMap, group=None) -> int:
+    """Max over ranks of ``m.halo_count()`` (torch.distributed all-reduce)."""
+    import torch.distributed as dist
+    everyone: list = [None] * m.nparts
+    dist.all_gather_object(everyone, m.halo_count(), group=group)
+    return int(max(everyone))
 
 
 def exchange_requests_local(maps: Sequence[DistMap]) -> None:
@@ -178,6 +201,49 @@ class Communicator:
         h = C.c_void_p()
         _check(lib.lbk_comm_init_nccl(uid, 1, 0, device, C.byref(h)))
         return Communicator(h, 1, 0, "nccl")
+
+    @staticmethod
+    def peer(device: int, halo_cap: int, group=None) -> "Communicator":
+        """One process per GPU on one node. ``halo_cap``: the max over ranks
+        of ``DistMap.halo_count()`` (see ``peer_halo_cap``)."""
+        import torch.distributed as dist
+        lib = L.load()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        h = C.c_void_p()
+        _check(lib.lbk_comm_init_peer(world, rank, device, int(halo_cap), C.byref(h)))
+        comm = Communicator(h, world, rank, "peer")
+        if world > 1:
+            mine = (C.c_char * 64)()
+            _check(lib.lbk_comm_peer_handle(h, mine))
+            allh: list = [None] * world
+            dist.all_gather_object(allh, bytes(mine), group=group)
+            buf = (C.c_char * (64 * world)).from_buffer_copy(b"".join(allh))
+            _check(lib.lbk_comm_peer_open(h, buf))
+            dist.barrier(group)
+        return comm
+
+    @staticmethod
+    def peer_group(devices: Sequence[int], halo_cap: int) -> list["Communicator"]:
+        lib = L.load()
+        n = len(devices)
+        dv = (C.c_int32 * n)(*devices)
+        arr = (C.c_void_p * n)()
+        _check(lib.lbk_comm_init_peer_group(n, dv, int(halo_cap), arr))
+        return [Communicator(C.c_void_p(arr[r]), n, r, "peer") for r in range(n)]
+
+    def close(self, group=None) -> None:
+        """Collective destroy: a peer window must stay mapped until every
+        rank is done with it."""
+        if self.kind == "peer" and self.nranks > 1:
+            import torch.distributed as dist
+            dist.barrier(group)
+        if getattr(self, "h", None):
+            self.lib.lbk_comm_destroy(self.h)
+            self.h = None
+
+    def sync(self, exec: CudaExecutor) -> None:
+        """Wait for the executor's stream; raise on a communicator failure."""
+        _check(self.lib.lbk_comm_sync(exec.ctx, self.h), exec.ctx)
 
     @staticmethod
     def threads(nranks: int) -> list["Communicator"]:
@@ -228,7 +294,10 @@ class DistCsrMatrix:
         _check(self.lib.lbk_dist_spmv_f64(self.exec.ctx, self.h, comm.h if comm else None,
                                           _ptr(x_ext), _ptr(y)), self.exec.ctx)
         if sync:
-            self.exec.synchronize()
+            if comm is not None:
+                comm.sync(self.exec)
+            else:
+                self.exec.synchronize()
 
     def solve(self, comm: Optional[Communicator], b: torch.Tensor, x: torch.Tensor,
               config: SolverConfig) -> SolveResult:

@@ -32,7 +32,11 @@ def build(O, lk, A, P, comm_kind="threads"):
     D.exchange_requests_local(maps)
     exs = [lk.CudaExecutor(0, stream=torch.cuda.Stream()) for _ in range(P)]
     mats = [D.DistCsrMatrix(exs[r], maps[r], parts[r][0], parts[r][1], A.nnz) for r in range(P)]
-    comms = D.Communicator.threads(P) if P > 1 else [None]
+    if comm_kind == "peer":
+        cap = max(m.halo_count() for m in maps)
+        comms = D.Communicator.peer_group([0] * P, cap)
+    else:
+        comms = D.Communicator.threads(P) if P > 1 else [None]
     return exs, mats, comms
 
 
@@ -171,3 +175,79 @@ def test_dist_cgs_gmres(O, lk, kind, P):
     x = np.concatenate([t.cpu().numpy() for t in xs])
     assert res[0].converged
     assert np.max(np.abs(O.spmv_csr(A, x) - b)) <= 1e-7 * np.max(np.abs(b))
+
+
+
+@pytest.fixture(scope="module", params=[2, 4])
+def peer_run(request, tmp_path_factory):
+    """P processes on cuda:0, one peer-memory rank each (tests/peer_worker.py):
+    one CUDA context per rank, windows swapped as CUDA IPC handles over
+    gloo -- the one-process-per-GPU deployment, with the GPUs folded onto
+    one device. (Ranks must not share a context: a kernel spinning on a
+    peer's flag would block device-synchronising calls of the other ranks'
+    host threads.)"""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    P = request.param
+    tmp = tmp_path_factory.mktemp(f"peer{P}")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    here = os.path.dirname(os.path.abspath(__file__))
+    procs = []
+    for r in range(P):
+        env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(r),
+                   WORLD_SIZE=str(P), LBK_PEER_TIMEOUT="120")
+        procs.append(subprocess.Popen([sys.executable, os.path.join(here, "peer_worker.py"),
+                                       str(tmp / f"r{r}.json")], env=env))
+    try:
+        codes = [p.wait(timeout=900) for p in procs]
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    assert codes == [0] * P, codes
+    return P, [json.loads((tmp / f"r{r}.json").read_text()) for r in range(P)]
+
+
+def test_peer_spmv_bitexact(peer_run):
+    P, out = peer_run
+    for o in out:
+        assert o["spmv_7pt"] and o["spmv_27pt"] and o["spmv_5pt"]
+        assert o["spmv_back_to_back"]
+        assert o["allreduce"] == [P * (P + 1) / 2, 0.25 * P]
+
+
+def test_peer_solvers(peer_run, O):
+    P, out = peer_run
+    for kind in ("cg", "bicgstab", "bicgstab_eager", "cgs", "gmres"):
+        r0 = out[0][kind]
+        for o in out[1:]:  # every rank: the same iterations and history bits
+            assert o[kind]["iters"] == r0["iters"] and o[kind]["hist"] == r0["hist"], kind
+        assert r0["conv"], kind
+    assert abs(out[0]["cg"]["iters"] - 81) <= 1  # golden (SURVEY.md §8c)
+    A = O.stencil("7pt", 32)
+    I = out[0]["cg"]["iters"]
+    assert out[0]["cg"]["flops"] == I * (4 * A.nnz + 16 * A.nrows) + 2 * A.nnz + 4 * A.nrows
+    x = np.concatenate([o["cg"]["x"] for o in out])
+    assert np.max(np.abs(x - 1.0)) < 1e-5
+    # captured graph and eager launches give the same bits
+    assert out[0]["bicgstab"]["hist"] == out[0]["bicgstab_eager"]["hist"]
+    A = O.stencil("7pt", 20, 0.5)
+    b = O.spmv_csr(A, O.seeded_values(A.nrows, 11))
+    x = np.concatenate([o["bicgstab"]["x"] for o in out])
+    assert np.max(np.abs(O.spmv_csr(A, x) - b)) <= 1e-7 * np.max(np.abs(b))
+    if O.ref_available():
+        rr = O.ref_solve(A, b, "bicgstab", rel_tol=1e-8, max_iters=20000)
+        rp = O.ref_solve(A, b, "bicgstab", rel_tol=1e-8, max_iters=20000, exec_kind=1, workers=8)
+        assert abs(out[0]["bicgstab"]["iters"] - rr.iterations) <= max(
+            1, abs(rp.iterations - rr.iterations))
+
+
+def test_peer_timeout_reported(peer_run):
+    P, out = peer_run
+    assert "timed out waiting for halo values" in out[0]["timeout"], out[0]["timeout"]
