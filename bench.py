@@ -48,6 +48,7 @@ if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
     os.environ["NCCL_DEBUG"] = "WARN"
 # a failed peer must cost minutes, not the driver's whole budget
 os.environ.setdefault("LBK_NCCL_TIMEOUT", "180")
+os.environ.setdefault("LBK_PEER_TIMEOUT", "120")
 
 METRIC = "FP64 CSR SpMV GB/s (% of HBM roofline) and CG iters/s at 1/2/4/8 B200"
 WORKLOAD = {"workload": "cfg2: FP64 CSR SpMV, 3D 27-pt Poisson 128^3 (2,097,152 rows, "
@@ -582,27 +583,42 @@ def run_cg(ex, world: int, rank: int, local_rank: int, force_dist: bool = False)
     except Exception:
         pass
     all_ok(m is not None, "partition maps")
+    # communicator: "peer" (default; halo and reductions in lbk's own kernels
+    # over IPC-mapped peer windows) or "nccl" (LBK_BENCH_COMM=nccl)
+    comm_kind = os.environ.get("LBK_BENCH_COMM", "peer")
     if world > 1:
         D.exchange_requests(m)
-        comm = D.Communicator.nccl(local_rank)
-    else:  # --cg-dist at N = 1: the same path on a one-rank NCCL communicator
+        if comm_kind == "nccl":
+            comm = D.Communicator.nccl(local_rank)
+        else:
+            comm = D.Communicator.peer(local_rank, D.peer_halo_cap(m))
+    else:  # --cg-dist at N = 1: the same path on a one-rank communicator
         D.exchange_requests_local([m])
-        comm = D.Communicator.nccl_single(local_rank)
+        if comm_kind == "nccl":
+            comm = D.Communicator.nccl_single(local_rank)
+        else:
+            comm = D.Communicator.peer_group([local_rank], m.halo_count())[0]
     M = None
     try:
         M = D.DistCsrMatrix(ex, m, rp, vals, nnz)
     except Exception:
         pass
     all_ok(M is not None, "device matrix")
-    cg["mode"] = (f"row-partitioned over {world} GPUs: NCCL halo exchange overlapped with the "
-                  f"interior rows, ncclAllReduce per reduction (strong scaling)")
+    if comm_kind == "nccl":
+        cg["mode"] = (f"row-partitioned over {world} GPUs: NCCL halo exchange overlapped with "
+                      f"the interior rows, ncclAllReduce per reduction (strong scaling)")
+    else:
+        cg["mode"] = (f"row-partitioned over {world} GPUs: halo stored into the neighbours' "
+                      f"peer windows before the interior rows, each reduction summed over the "
+                      f"peers in one kernel (strong scaling)")
+    cg["comm"] = comm_kind
     cg["n_ghost_rank0"] = M.n_ghost
     for mode in ("true", "recurrence"):
         x = torch.zeros(M.n_local, dtype=torch.float64, device=dev)
         torch.cuda.synchronize()
         # warm-up: module loading and the CUDA-graph capture of a chunk
         M.solve(comm, b_loc, torch.zeros(M.n_local, dtype=torch.float64, device=dev),
-                lk.SolverConfig(kind="cg", rel_tol=1e-8, fixed_iters=40, residual_mode=mode))
+                lk.SolverConfig(kind="cg", rel_tol=1e-8, max_iters=40, residual_mode=mode))
         torch.cuda.synchronize()
         r = M.solve(comm, b_loc, x, lk.SolverConfig(kind="cg", rel_tol=1e-8, max_iters=20000,
                                                      residual_mode=mode))
@@ -610,6 +626,7 @@ def run_cg(ex, world: int, rank: int, local_rank: int, force_dist: bool = False)
         cg[mode] = {"iterations": r.iterations, "final_rel_residual": r.final_rel_residual,
                     "seconds": el, "iters_per_s": r.iterations / el, "flop_count": r.flop_count,
                     "gflops_ref_model": r.flop_count / el / 1e9}
+    comm.close()  # collective: peers may still be storing into this rank's window
     return cg
 
 
