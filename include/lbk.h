@@ -369,9 +369,12 @@ lbk_status lbk_dist_csr_create(lbk_ctx ctx, lbk_dist_map m, const int32_t* row_p
                                const double* vals, int64_t n_global_nnz, lbk_dist_csr* out);
 lbk_status lbk_dist_csr_info(lbk_dist_csr D, int32_t* n_local, int32_t* n_ghost);
 lbk_status lbk_dist_csr_destroy(lbk_dist_csr D);
-/* y[n_local] <- A x; x_ext[n_local + n_ghost] (halo filled by the call):
- * pack -> ncclSend/ncclRecv on a comm stream overlapped with the interior
- * rows -> boundary rows.  Collective: every rank calls it. */
+/* y[n_local] <- A x; x_ext[n_local + n_ghost] (halo filled by the call).
+ * Peer communicator: pack + store into the neighbours' windows -> interior
+ * rows -> wait + unpack -> boundary rows, all on the context's stream.
+ * NCCL: pack -> ncclSend/ncclRecv on a comm stream overlapped with the
+ * interior rows -> boundary rows.  Collective: every rank calls it, on the
+ * same context stream every time (the peer epochs are per stream order). */
 lbk_status lbk_dist_spmv_f64(lbk_ctx ctx, lbk_dist_csr D, lbk_comm comm, double* x_ext, double* y);
 /* Distributed solve (CG / BiCGSTAB, lbk_solver_cfg as lbk_solve_csr): b, x
  * are the rank's n_local parts; dot products are reduced over ranks, so
