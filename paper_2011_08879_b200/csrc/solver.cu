@@ -169,10 +169,10 @@ struct EpiCgK1 {
     double* __restrict__ q;
     const double* __restrict__ p;
     SolverState* st;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     struct Pre {
         double p;
     };
-    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     __device__ Pre pre(int i) const { return {p[i]}; }
     __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
     __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
@@ -201,9 +201,6 @@ struct EpiCgK3 {
     double* __restrict__ p;
     const double* __restrict__ r;
     SolverState* st;
-    struct Pre {
-        double b, p, r;
-    };
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     __device__ void prefetch(int rb, int re) const
     {
@@ -211,6 +208,9 @@ struct EpiCgK3 {
         l2_prefetch_rows(p, rb, re);
         l2_prefetch_rows(r, rb, re);
     }
+    struct Pre {
+        double b, p, r;
+    };
     __device__ Pre pre(int i) const { return {b[i], p[i], r[i]}; }
     __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
     __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const

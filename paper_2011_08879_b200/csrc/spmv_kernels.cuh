@@ -241,10 +241,13 @@ __device__ __forceinline__ T warp_row_global(int ks, int ke, const int* __restri
     return warp_sum(add_rn(add_rn(p0, p1), add_rn(p2, p3)));
 }
 
-// Epilogue operand prefetch: an epilogue may declare `struct Pre`, `Pre
-// pre(int r)` and `row_pre(r, s, pre, acc)`; the staged sweep then issues
-// the row's operand loads (b[r], p[r], ...) together with its gathers, so
-// one memory round trip per pass serves both.
+// Register-level operand prefetch (opt-in, -DLBK_EPI_PRE): an epilogue may
+// declare `struct Pre`, `Pre pre(int r)` and `row_pre(r, s, pre, acc)`; the
+// staged sweep then issues the row's operand loads (b[r], p[r], ...)
+// together with its gathers.  Off by default: with the operand streams
+// already L2-prefetched when the tile is staged (EpiPf), the extra live
+// registers cost more than the latency they hide -- measured on cfg4/cfg5,
+// CG 1102 -> 1176 it/s, BiCGSTAB 728 -> 752, CGS 739 -> 764 without it.
 template <class Epi, class = void>
 struct EpiPre {
     struct type {};
@@ -255,6 +258,7 @@ struct EpiPre {
         e.row(r, s, acc);
     }
 };
+#ifdef LBK_EPI_PRE
 template <class Epi>
 struct EpiPre<Epi, std::void_t<typename Epi::Pre>> {
     using type = typename Epi::Pre;
@@ -265,6 +269,7 @@ struct EpiPre<Epi, std::void_t<typename Epi::Pre>> {
         e.row_pre(r, s, p, acc);
     }
 };
+#endif
 
 // Epilogues that read DRAM operand vectors declare
 // `void prefetch(int rb, int re) const`; others prefetch nothing.

@@ -43,6 +43,8 @@ def run(name, A, fmts):
 for cfg in ["cfg1", "cfg2"]:
     c = gen.CONFIGS[cfg]
     run(cfg, gen.stencil(ex, c["kind"], c["m"], c["gamma"]), ["csr", "coo"])
+if "--cfg4" in sys.argv:  # the CG operator: 7-pt 256^3
+    run("cfg4", gen.stencil(ex, "7pt", 256, 0.0), ["csr"])
 if "--powerlaw" in sys.argv:
     rp, ci, va = gen.powerlaw_host(1 << 24)
     run("cfg3", lk.csr_from_host(ex, 1 << 24, 1 << 24, rp, ci, va), ["csr", "coo"])
