@@ -706,6 +706,12 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # dev-only: LBK_BENCH_FOLD=1 folds every rank onto cuda:0 (gloo
+    # bootstrap) to exercise the N > 1 code paths on a one-GPU box; its
+    # numbers are meaningless (the ranks' contexts time-slice)
+    fold = os.environ.get("LBK_BENCH_FOLD") == "1"
+    if fold:
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank)
         return
@@ -714,8 +720,11 @@ def main() -> None:
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         import datetime
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank),
-                                timeout=datetime.timedelta(minutes=5))
+        if fold:
+            dist.init_process_group("gloo", timeout=datetime.timedelta(minutes=10))
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank),
+                                    timeout=datetime.timedelta(minutes=5))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
