@@ -1,0 +1,126 @@
+"""Summarise one gpu_round.sh session into profiles/ (tracked).
+
+    python scripts/summarize_profiles.py TAG ROUND
+
+reads gpurun_out/TAG_{launches.csv,csr.ncu-rep,cg.ncu-rep,bench.json,
+bench_ref.json,pytest_gpu.log} and writes profiles/rROUND_launches_summary.txt,
+rROUND_csr_stream_ncu_full.txt, rROUND_cg_kernels_ncu.txt,
+rROUND_bench_N1.json, rROUND_bench_reference_N1.json and ncu_summary.json
+(the roofline `traffic` source read by bench.py)."""
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+tag, rnd = sys.argv[1], int(sys.argv[2])
+G = os.path.join(ROOT, "gpurun_out")
+P = os.path.join(ROOT, "profiles")
+CSR_BYTES = 710858660  # cfg2: 12 nnz + 4 (n + 1) + 16 n
+
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+           "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+           "lts__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
+           "smsp__issue_active.avg.pct_of_peak_sustained_active",
+           "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+           "launch__shared_mem_per_block_dynamic"]
+
+
+def launches():
+    rows = list(csv.reader(open(os.path.join(G, f"{tag}_launches.csv"))))
+    hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    h = rows[hdr]
+    agg = collections.OrderedDict()
+    for r in rows[hdr + 1:]:
+        if len(r) != len(h):
+            continue
+        d = dict(zip(h, r))
+        if d["Metric Name"] != "gpu__time_duration.sum":
+            continue
+        v = float(d["Metric Value"].replace(",", ""))
+        us = v / 1e3 if d["Metric Unit"] == "nsecond" else (v if d["Metric Unit"] == "usecond"
+                                                             else v * 1e3)
+        a = agg.setdefault(d["Kernel Name"], [0, 0.0])
+        a[0] += 1
+        a[1] += us
+    tot = sum(a[1] for a in agg.values())
+    out = [f"# ncu --metrics gpu__time_duration.sum --clock-control none -c 400 python bench.py "
+           f"--steps 20 --warmup 3 --no-cpu --no-formats",
+           "# cold-cache, serialised launches: compare SHARES, not absolutes. First 400 launches: "
+           "device stencil gen, bench SpMV steps (cfg2), e2e steps, then the CG cfg4 kernels.",
+           "launches     total_us     avg_us  share  kernel"]
+    for k, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        out.append(f"{n:8d} {us:12.1f} {us / n:10.1f} {100 * us / tot:5.1f}%  {k}")
+    open(os.path.join(P, f"r{rnd}_launches_summary.txt"), "w").write("\n".join(out) + "\n")
+
+
+def raw(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    h, units = rows[0], rows[1]
+    return [(dict(zip(h, r)), dict(zip(h, units))) for r in rows[2:] if len(r) == len(h)]
+
+
+def fmt(d, u, m):
+    return f"{m} = {d.get(m, '?')} {u.get(m, '')}".rstrip()
+
+
+def to_bytes(d, u, m):
+    v = float(d[m].replace(",", ""))
+    return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u[m], 1)
+
+
+def csr_full():
+    rep = os.path.join(G, f"{tag}_csr.ncu-rep")
+    (d, u), = raw(rep)[:1]
+    dram = to_bytes(d, u, "dram__bytes_read.sum") + to_bytes(d, u, "dram__bytes_write.sum")
+    dur = float(d["gpu__time_duration.sum"].replace(",", ""))
+    dur_us = dur / 1e3 if u["gpu__time_duration.sum"] == "nsecond" else dur
+    lines = ["# ncu --set full --clock-control none --import-source on -k regex:csr_stream -s 5 "
+             "-c 1 python bench.py --steps 8 --warmup 3 --no-cg --no-cpu --no-formats",
+             f"# kernel: {d['Kernel Name']}",
+             f"# workload: cfg2 CSR SpMV (27-pt 128^3, 55,742,968 nnz); algorithmic bytes/launch "
+             f"{CSR_BYTES:,}"]
+    lines += [fmt(d, u, m) for m in METRICS]
+    lines.append(f"dram_bytes_total = {int(dram)} B  (traffic / algorithmic = "
+                 f"{dram / CSR_BYTES:.3f}; x is L2-resident)")
+    open(os.path.join(P, f"r{rnd}_csr_stream_ncu_full.txt"), "w").write("\n".join(lines) + "\n")
+    json.dump({"round": rnd, "source": f"profiles/r{rnd}_csr_stream_ncu_full.txt",
+               "kernels": {"csr_stream_kernel": {
+                   "config": "cfg2", "dram_bytes_per_launch": int(dram),
+                   "algorithmic_bytes_per_launch": CSR_BYTES, "ncu_duration_us": dur_us}}},
+              open(os.path.join(P, "ncu_summary.json"), "w"), indent=1)
+
+
+def cg_full():
+    rep = os.path.join(G, f"{tag}_cg.ncu-rep")
+    if not os.path.exists(rep):
+        return
+    lines = ["# ncu --set full --clock-control none -k regex:'csr_stream|vec_kernel' "
+             "python scripts/prof_k1.py: plain cfg4 CSR SpMV, then 2 CG iterations (cfg4, 7-pt "
+             "256^3): EpiInit, K1, K2, K3"]
+    for d, u in raw(rep):
+        lines.append(f"\n[{d['Kernel Name'][:150]}]")
+        lines += ["  " + fmt(d, u, m) for m in METRICS]
+    open(os.path.join(P, f"r{rnd}_cg_kernels_ncu.txt"), "w").write("\n".join(lines) + "\n")
+
+
+def bench():
+    for src, dst in ((f"{tag}_bench.json", f"r{rnd}_bench_N1.json"),
+                     (f"{tag}_bench_ref.json", f"r{rnd}_bench_reference_N1.json")):
+        lines = [ln for ln in open(os.path.join(G, src)).read().splitlines()
+                 if ln.startswith("{")]
+        if lines:
+            json.dump(json.loads(lines[-1]), open(os.path.join(P, dst), "w"), indent=1)
+
+
+launches()
+csr_full()
+cg_full()
+bench()
+print("ok")
