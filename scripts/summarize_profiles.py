@@ -1,6 +1,6 @@
 """Summarise one gpu_round.sh session into profiles/ (tracked).
 
-    python scripts/summarize_profiles.py TAG ROUND
+    python scripts/summarize_profiles.py TAG ROUND [OUTDIR]
 
 reads gpurun_out/TAG_{launches.csv,csr.ncu-rep,cg.ncu-rep,bench.json,
 bench_ref.json,pytest_gpu.log} and writes profiles/rROUND_launches_summary.txt,
@@ -16,9 +16,11 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-tag, rnd = sys.argv[1], int(sys.argv[2])
+tag, rnd = sys.argv[1], int(sys.argv[2])  # noqa: E501
 G = os.path.join(ROOT, "gpurun_out")
-P = os.path.join(ROOT, "profiles")
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+P = args[2] if len(args) > 2 else os.path.join(ROOT, "profiles")
+os.makedirs(P, exist_ok=True)
 CSR_BYTES = 710858660  # cfg2: 12 nnz + 4 (n + 1) + 16 n
 
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -42,8 +44,9 @@ def launches():
         if d["Metric Name"] != "gpu__time_duration.sum":
             continue
         v = float(d["Metric Value"].replace(",", ""))
-        us = v / 1e3 if d["Metric Unit"] == "nsecond" else (v if d["Metric Unit"] == "usecond"
-                                                             else v * 1e3)
+        scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3,
+                 "msecond": 1e3}
+        us = v * scale[d["Metric Unit"]]
         a = agg.setdefault(d["Kernel Name"], [0, 0.0])
         a[0] += 1
         a[1] += us
@@ -120,7 +123,8 @@ def bench():
 
 
 launches()
-csr_full()
-cg_full()
-bench()
+if "--launches-only" not in sys.argv:
+    csr_full()
+    cg_full()
+    bench()
 print("ok")
