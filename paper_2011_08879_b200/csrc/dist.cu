@@ -223,6 +223,7 @@ struct PeerComm final : Comm {
         need(ready, LBK_USAGE_ERROR, "peer communicator: peers not opened yet");
         return &pd;
     }
+    void set_ready() { ready = true; }
     void allreduce_sum(double* dev, int count, cudaStream_t s) override;
     void exchange(const double*, const std::vector<int>&, double*, const std::vector<int>&,
                   cudaStream_t) override
@@ -267,7 +268,6 @@ struct PeerComm final : Comm {
         LBK_CUDA(cudaMemcpy(local, &h, sizeof(h), cudaMemcpyHostToDevice));
         pd.P = P;
         pd.rank = r;
-        pd.debug = std::getenv("LBK_PEER_DEBUG") ? 1 : 0;
         pd.cap = cap;
         pd.win[r] = local;
     }
@@ -288,7 +288,7 @@ __global__ void peer_allreduce_kernel(PeerDev pd, double* dev, int count)
 {
     const int lane = threadIdx.x;
     const double v = lane < count ? dev[lane] : 0.0;
-    const double t = peer_allreduce_warp(pd, v, count);
+    const double t = peer_allreduce_warp(pd, v, count > 0 ? count : 1);
     if (lane < count) dev[lane] = t;
 }
 
@@ -336,7 +336,6 @@ __global__ void peer_push_kernel(PeerDev pd, const int* __restrict__ send_off,
             __threadfence_system();
             for (int q = 0; q < pd.P; ++q)
                 if (so[q + 1] > so[q]) st_release_sys(&pd.win[q]->full[pd.rank], e);
-            if (pd.debug) printf("[peer] rank %d push epoch %llu n %d\n", pd.rank, e, ns);
         }
     }
 }
@@ -369,7 +368,6 @@ __global__ void peer_recv_kernel(PeerDev pd, const int* __restrict__ recv_off,
             for (int q = 0; q < pd.P; ++q)
                 if (ro[q + 1] > ro[q]) st_release_sys(&pd.win[q]->empty[pd.rank], e);
             *reinterpret_cast<volatile unsigned long long*>(&me->seq_x) = e;
-            if (pd.debug) printf("[peer] rank %d recv epoch %llu n %d\n", pd.rank, e, nr);
         }
     }
 }
@@ -673,7 +671,7 @@ lbk_status lbk_comm_init_peer(int32_t nranks, int32_t rank, int32_t device, int6
     return guard(nullptr, [&] {
         auto c = std::make_unique<PeerComm>();
         c->create(nranks, rank, device, halo_cap);
-        if (nranks == 1) c->ready = true;
+        if (nranks == 1) c->set_ready();
         auto h = std::make_unique<lbk_comm_s>();
         h->impl = c.release();
         *out = h.release();
@@ -710,7 +708,7 @@ lbk_status lbk_comm_peer_open(lbk_comm comm, const void* handles)
             c->pd.win[q] = static_cast<PeerHdr*>(p);
         }
         c->verify_caps();
-        c->ready = true;
+        c->set_ready();
     });
 }
 
@@ -747,7 +745,7 @@ lbk_status lbk_comm_init_peer_group(int32_t nranks, const int32_t* devices, int6
                 }
             }
         for (int r = 0; r < nranks; ++r) {
-            cs[r]->ready = true;
+            cs[r]->set_ready();
             auto h = std::make_unique<lbk_comm_s>();
             h->impl = cs[r].release();
             comms_out[r] = h.release();

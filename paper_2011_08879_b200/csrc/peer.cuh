@@ -37,8 +37,10 @@ constexpr int kPeerRedMax = 16;  // values per reduction
 struct PeerHdr {
     unsigned long long full[kPeerMax];   // halo epoch rank q pushed into me
     unsigned long long empty[kPeerMax];  // halo epoch rank q consumed from me
-    unsigned long long redf[kPeerMax];   // reduction epoch rank q posted to me
-    double red[2][kPeerMax][kPeerRedMax];
+    // reduction mailbox, LL-style: each double travels as two 8-byte words
+    // {epoch:32 | half:32}, [parity][source rank][value][half]; a word is
+    // valid when its epoch tag matches, so no fences or flags are needed
+    unsigned long long red_ll[2][kPeerMax][kPeerRedMax][2];
     unsigned long long seq_x, seq_r;     // local epochs (this rank only)
     unsigned int push_cnt, recv_cnt;     // last-block counters
     int error;
@@ -56,7 +58,6 @@ struct PeerDev {
     PeerHdr* win[kPeerMax];
     int P = 0, rank = 0;
     long long cap = 0;
-    int debug = 0;  // LBK_PEER_DEBUG: device printf of every epoch
     // staging slot (parity par, source src) inside rank q's window
     __device__ double* stage(int q, int par, int src) const
     {
@@ -104,39 +105,71 @@ __device__ __forceinline__ void peer_wait_ge(const unsigned long long* f, unsign
     }
 }
 
-// One warp.  Lane i < n contributes v; returns the rank-ordered sum over
-// all ranks in lane i (identical bits on every rank).
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p)
+{
+    unsigned long long v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v)
+{
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Read one LL-encoded double posted with epoch tag e32 (spin until both
+// halves carry the tag, the group fails, or the timeout expires).
+__device__ __forceinline__ double peer_ll_read(const unsigned long long* w, unsigned e32,
+                                               PeerHdr* me, int peer, unsigned long long e)
+{
+    unsigned long long a = ld_volatile_u64(w), b = ld_volatile_u64(w + 1);
+    if (static_cast<unsigned>(a >> 32) != e32 || static_cast<unsigned>(b >> 32) != e32) {
+        const unsigned long long t0 = global_ns();
+        for (;;) {
+            a = ld_volatile_u64(w);
+            b = ld_volatile_u64(w + 1);
+            if (static_cast<unsigned>(a >> 32) == e32 && static_cast<unsigned>(b >> 32) == e32)
+                break;
+            if (*reinterpret_cast<volatile int*>(&me->error)) break;
+            if (global_ns() - t0 > static_cast<unsigned long long>(me->timeout_ns)) {
+                if (atomicExch(&me->error, 1) == 0) {
+                    me->err_info[0] = 2;
+                    me->err_info[1] = peer;
+                    me->err_info[2] = static_cast<long long>(e);
+                    me->err_info[3] = static_cast<long long>(a >> 32);
+                }
+                break;
+            }
+            __nanosleep(32);
+        }
+    }
+    return __longlong_as_double(static_cast<long long>((b << 32) | (a & 0xffffffffull)));
+}
+
+// One warp.  Lane i < n (1 <= n <= kPeerRedMax) contributes v; returns the
+// rank-ordered sum over all ranks in lane i (identical bits on every rank).
+// Every rank reads every other rank's post of this epoch before it can
+// post the next, so no rank runs two epochs ahead and parity reuse is safe.
 __device__ __forceinline__ double peer_allreduce_warp(const PeerDev& pd, double v, int n)
 {
     const int lane = threadIdx.x & 31;
     PeerHdr* me = pd.win[pd.rank];
     const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&me->seq_r) + 1;
     const int par = static_cast<int>(e & 1);
+    const unsigned e32 = static_cast<unsigned>(e);
+    const unsigned long long tag = static_cast<unsigned long long>(e32) << 32;
+    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
     if (lane < n)
-        for (int q = 0; q < pd.P; ++q)
-            *reinterpret_cast<volatile double*>(&pd.win[q]->red[par][pd.rank][lane]) = v;
-    __threadfence_system();
-    __syncwarp();
-    if (lane == 0)
-        for (int q = 0; q < pd.P; ++q) st_release_sys(&pd.win[q]->redf[pd.rank], e);
-    // every lane waits for every post (local loads): no rank can run two
-    // epochs ahead of another, which is what makes parity reuse safe
-    for (int q = 0; q < pd.P; ++q) peer_wait_ge(&me->redf[q], e, me, 2, q);
+        for (int q = 0; q < pd.P; ++q) {
+            unsigned long long* w = pd.win[q]->red_ll[par][pd.rank][lane];
+            st_volatile_u64(w, tag | (bits & 0xffffffffull));
+            st_volatile_u64(w + 1, tag | (bits >> 32));
+        }
     double t = 0.0;
     if (lane < n)
         for (int q = 0; q < pd.P; ++q)
-            t = add_rn(t, *reinterpret_cast<volatile double*>(&me->red[par][q][lane]));
+            t = add_rn(t, peer_ll_read(me->red_ll[par][q][lane], e32, me, q, e));
     __syncwarp();
-    if (lane == 0) {
-        *reinterpret_cast<volatile unsigned long long*>(&me->seq_r) = e;
-        if (pd.debug)
-            printf("[peer] rank %d reduce epoch %llu n %d sum0 %.17g flags %llu %llu err %d "
-                   "vals %.17g %.17g\n",
-                   pd.rank, e, n, t, ld_acquire_sys(&me->redf[0]),
-                   pd.P > 1 ? ld_acquire_sys(&me->redf[1]) : 0ull, me->error,
-                   *reinterpret_cast<volatile double*>(&me->red[par][0][0]),
-                   pd.P > 1 ? *reinterpret_cast<volatile double*>(&me->red[par][1][0]) : 0.0);
-    }
+    if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(&me->seq_r) = e;
     return t;
 }
 

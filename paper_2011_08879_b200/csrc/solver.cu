@@ -1114,10 +1114,7 @@ __global__ void finish_kernel(E e, const double* tot)
 template <class E>
 __global__ void peer_finish_kernel(E e, const double* base, int has_a, int has_b, PeerDev pd)
 {
-    if (e.skip()) {
-        if (pd.debug && threadIdx.x == 0) printf("[peer] rank %d finish skipped\n", pd.rank);
-        return;
-    }
+    if (e.skip()) return;
     static_assert(E::NV <= 8, "peer finish: at most 8 values");
     const int lane = threadIdx.x;
     double v = 0.0;
@@ -1125,7 +1122,7 @@ __global__ void peer_finish_kernel(E e, const double* base, int has_a, int has_b
         if (has_a) v = add_rn(v, base[lane]);
         if (has_b) v = add_rn(v, base[8 + lane]);
     }
-    const double t = peer_allreduce_warp(pd, v, E::NV);
+    const double t = peer_allreduce_warp(pd, v, E::NV > 0 ? E::NV : 1);
     __shared__ double tot[8];
     if (lane < E::NV) tot[lane] = t;
     __syncwarp();
@@ -1156,6 +1153,7 @@ struct DistEnv {
     template <class E>
     void finish(const E& e, int has_a, int has_b)
     {
+        // peer group: combine + the rank sum + finish() in one launch
         if (const PeerDev* pd = comm ? comm->peer() : nullptr) {
             peer_finish_kernel<E><<<1, 32, 0, ctx->stream>>>(e, ws.out, has_a, has_b, *pd);
             LBK_LAUNCH_CHECK();
