@@ -256,7 +256,7 @@ struct PeerComm final : Comm {
         rank = r;
         device = dev;
         LBK_CUDA(cudaSetDevice(dev));
-        const size_t bytes = kPeerHdrBytes + size_t(2) * P * size_t(cap) * sizeof(double);
+        const size_t bytes = kPeerHdrBytes + size_t(2) * P * size_t(cap) * 2 * sizeof(double);
         LBK_CUDA(cudaMallocHost(&err_host, sizeof(int)));
         *err_host = 0;
         LBK_CUDA(cudaMalloc(&local, bytes));
@@ -309,8 +309,9 @@ __device__ __forceinline__ int seg_of(const int* off, int P, int i)
     return q;
 }
 
-// gather x[send_idx] and store each peer's run into its staging slot
-// (parity e & 1, source = this rank), then raise the peers' `full` flags
+// gather x[send_idx] and store each peer's run, LL-tagged with the halo
+// epoch, into its staging slot (parity e & 1, source = this rank) -- once
+// the receiver has handed back the slot's previous epoch
 __global__ void peer_push_kernel(PeerDev pd, const int* __restrict__ send_off,
                                  const int* __restrict__ send_idx, const double* __restrict__ x)
 {
@@ -318,6 +319,7 @@ __global__ void peer_push_kernel(PeerDev pd, const int* __restrict__ send_off,
     PeerHdr* me = pd.win[pd.rank];
     const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&me->seq_x) + 1;
     const int par = static_cast<int>(e & 1);
+    const unsigned long long tag = (e & 0xffffffffull) << 32;
     if (threadIdx.x <= pd.P) so[threadIdx.x] = send_off[threadIdx.x];
     __syncthreads();
     const int q0 = threadIdx.x;
@@ -326,21 +328,12 @@ __global__ void peer_push_kernel(PeerDev pd, const int* __restrict__ send_off,
     const int ns = so[pd.P];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) {
         const int q = seg_of(so, pd.P, i);
-        pd.stage(q, par, pd.rank)[i - so[q]] = x[__ldg(send_idx + i)];
-    }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (atomicAdd(&me->push_cnt, 1u) == gridDim.x - 1) {
-            me->push_cnt = 0;
-            __threadfence_system();
-            for (int q = 0; q < pd.P; ++q)
-                if (so[q + 1] > so[q]) st_release_sys(&pd.win[q]->full[pd.rank], e);
-        }
+        peer_ll_store(pd.stage(q, par, pd.rank) + 2 * size_t(i - so[q]), x[__ldg(send_idx + i)],
+                      tag);
     }
 }
 
-// wait for the neighbours' pushes of epoch e, copy the staged ghosts behind
+// read the neighbours' tagged values of epoch e into the ghosts behind
 // x_local, hand the slots back, advance the halo epoch
 __global__ void peer_recv_kernel(PeerDev pd, const int* __restrict__ recv_off,
                                  double* __restrict__ ghost)
@@ -351,22 +344,20 @@ __global__ void peer_recv_kernel(PeerDev pd, const int* __restrict__ recv_off,
     const int par = static_cast<int>(e & 1);
     if (threadIdx.x <= pd.P) ro[threadIdx.x] = recv_off[threadIdx.x];
     __syncthreads();
-    const int q0 = threadIdx.x;
-    if (q0 < pd.P && ro[q0 + 1] > ro[q0]) peer_wait_ge(&me->full[q0], e, me, 0, q0);
-    __syncthreads();
     const int nr = ro[pd.P];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x) {
         const int q = seg_of(ro, pd.P, i);
-        ghost[i] = __ldcv(pd.stage(pd.rank, par, q) + (i - ro[q]));
+        ghost[i] = peer_ll_read(pd.stage(pd.rank, par, q) + 2 * size_t(i - ro[q]),
+                                static_cast<unsigned>(e), me, 0, q, e);
     }
-    __threadfence();
+    // every value read has been consumed (stored) above: the slot may be
+    // overwritten as soon as the senders see the hand-back
     __syncthreads();
     if (threadIdx.x == 0) {
         if (atomicAdd(&me->recv_cnt, 1u) == gridDim.x - 1) {
             me->recv_cnt = 0;
-            __threadfence_system();
             for (int q = 0; q < pd.P; ++q)
-                if (ro[q + 1] > ro[q]) st_release_sys(&pd.win[q]->empty[pd.rank], e);
+                if (ro[q + 1] > ro[q]) st_volatile_u64(&pd.win[q]->empty[pd.rank], e);
             *reinterpret_cast<volatile unsigned long long*>(&me->seq_x) = e;
         }
     }

@@ -4,24 +4,28 @@
 // handle; in-process groups share the pointer).  Every rank maps every
 // peer's window, so the two collectives of the distributed solver are plain
 // loads and stores over NVLink issued by lbk's own kernels -- no NCCL on
-// the iteration path, no host involvement, and CUDA-graph capturable:
+// the iteration path, no host involvement, and CUDA-graph capturable.
+//
+// Both use LL-style words (as NCCL's low-latency protocol): a double
+// travels as two 8-byte stores {epoch:32 | half:32}; a reader spins until
+// both halves carry the epoch it expects.  No fences, no separate flags --
+// an 8-byte store arrives whole, and the tag says which epoch it belongs to.
 //
 //   halo     the pack kernel gathers the values a peer needs and stores
-//            them straight into that peer's staging slot, then raises the
-//            peer's `full` flag; after the interior rows, the receive kernel
-//            waits for the flags of its neighbours, copies the staged ghosts
-//            behind x_local and hands the slot back (`empty` flag in the
-//            sender's window).
+//            them, tagged, straight into that peer's staging slot; after
+//            the interior rows, the receive kernel waits for each word's
+//            tag, writes the ghosts behind x_local and hands the slot back
+//            (`empty` word in the sender's window).
 //   scalars  the finishing kernel of each fused reduction posts the rank's
-//            totals into every window's `red` slot, waits for all P posts
-//            and sums them in rank order -- the same bits on every rank --
-//            then advances the solver recurrence (combine + allreduce +
-//            finish in one launch).
+//            totals into every window's mailbox, waits for all P posts and
+//            sums them in rank order -- the same bits on every rank -- then
+//            advances the solver recurrence (combine + allreduce + finish
+//            in one launch).
 //
 // Epochs are device counters (seq_x, seq_r) so captured graphs replay
-// correctly.  Slots are double-buffered by epoch parity: a sender may only
-// reuse a halo slot once the receiver has consumed the epoch before last
-// (`empty`); a reduction slot of parity p is rewritten two epochs later,
+// correctly.  Slots are double-buffered by epoch parity: a sender reuses a
+// halo slot only once the receiver has consumed the epoch before last
+// (`empty`); a mailbox slot of parity p is rewritten two epochs later,
 // which every rank can only reach after all ranks have read it.  Waits spin
 // with a timeout (LBK_PEER_TIMEOUT seconds, default 300); a timeout raises
 // the sticky `error` word that the host reports as LBK_NCCL_ERROR.
@@ -35,20 +39,21 @@ constexpr int kPeerMax = 16;     // ranks per peer group (one NVSwitch node)
 constexpr int kPeerRedMax = 16;  // values per reduction
 
 struct PeerHdr {
-    unsigned long long full[kPeerMax];   // halo epoch rank q pushed into me
     unsigned long long empty[kPeerMax];  // halo epoch rank q consumed from me
     // reduction mailbox, LL-style: each double travels as two 8-byte words
     // {epoch:32 | half:32}, [parity][source rank][value][half]; a word is
     // valid when its epoch tag matches, so no fences or flags are needed
     unsigned long long red_ll[2][kPeerMax][kPeerRedMax][2];
     unsigned long long seq_x, seq_r;     // local epochs (this rank only)
-    unsigned int push_cnt, recv_cnt;     // last-block counters
+    unsigned int recv_cnt, pad0_;        // last-block counter
     int error;
     int pad_;
-    long long err_info[4];  // first timeout: {what (0 halo full, 1 halo empty,
-                            // 2 reduction), peer, wanted epoch, seen epoch}
+    long long err_info[4];  // first timeout: {what (0 halo values, 1 halo
+                            // hand-back, 2 reduction), peer, wanted epoch,
+                            // seen epoch}
     long long timeout_ns;
     long long cap;  // halo values per (parity, source) slot -- equal on all ranks
+    // staging after the header: [parity][source][cap][2] LL words
 };
 
 constexpr size_t kPeerHdrBytes = (sizeof(PeerHdr) + 255) / 256 * 256;
@@ -59,22 +64,23 @@ struct PeerDev {
     int P = 0, rank = 0;
     long long cap = 0;
     // staging slot (parity par, source src) inside rank q's window
-    __device__ double* stage(int q, int par, int src) const
+    __device__ unsigned long long* stage(int q, int par, int src) const
     {
-        return reinterpret_cast<double*>(reinterpret_cast<char*>(win[q]) + kPeerHdrBytes) +
-               (static_cast<size_t>(par) * P + src) * cap;
+        return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(win[q]) +
+                                                     kPeerHdrBytes) +
+               (static_cast<size_t>(par) * P + src) * cap * 2;
     }
 };
 
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p)
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p)
 {
     unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v)
+__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v)
 {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long global_ns()
 {
@@ -87,10 +93,10 @@ __device__ __forceinline__ unsigned long long global_ns()
 __device__ __forceinline__ void peer_wait_ge(const unsigned long long* f, unsigned long long e,
                                              PeerHdr* me, int what, int peer)
 {
-    if (ld_acquire_sys(f) >= e) return;
+    if (ld_volatile_u64(f) >= e) return;
     const unsigned long long t0 = global_ns();
     unsigned long long seen;
-    while ((seen = ld_acquire_sys(f)) < e) {
+    while ((seen = ld_volatile_u64(f)) < e) {
         if (*reinterpret_cast<volatile int*>(&me->error)) return;
         if (global_ns() - t0 > static_cast<unsigned long long>(me->timeout_ns)) {
             if (atomicExch(&me->error, 1) == 0) {
@@ -105,21 +111,12 @@ __device__ __forceinline__ void peer_wait_ge(const unsigned long long* f, unsign
     }
 }
 
-__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p)
-{
-    unsigned long long v;
-    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v)
-{
-    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 
 // Read one LL-encoded double posted with epoch tag e32 (spin until both
 // halves carry the tag, the group fails, or the timeout expires).
 __device__ __forceinline__ double peer_ll_read(const unsigned long long* w, unsigned e32,
-                                               PeerHdr* me, int peer, unsigned long long e)
+                                               PeerHdr* me, int what, int peer,
+                                               unsigned long long e)
 {
     unsigned long long a = ld_volatile_u64(w), b = ld_volatile_u64(w + 1);
     if (static_cast<unsigned>(a >> 32) != e32 || static_cast<unsigned>(b >> 32) != e32) {
@@ -132,7 +129,7 @@ __device__ __forceinline__ double peer_ll_read(const unsigned long long* w, unsi
             if (*reinterpret_cast<volatile int*>(&me->error)) break;
             if (global_ns() - t0 > static_cast<unsigned long long>(me->timeout_ns)) {
                 if (atomicExch(&me->error, 1) == 0) {
-                    me->err_info[0] = 2;
+                    me->err_info[0] = what;
                     me->err_info[1] = peer;
                     me->err_info[2] = static_cast<long long>(e);
                     me->err_info[3] = static_cast<long long>(a >> 32);
@@ -143,6 +140,14 @@ __device__ __forceinline__ double peer_ll_read(const unsigned long long* w, unsi
         }
     }
     return __longlong_as_double(static_cast<long long>((b << 32) | (a & 0xffffffffull)));
+}
+
+__device__ __forceinline__ void peer_ll_store(unsigned long long* w, double v,
+                                              unsigned long long tag)
+{
+    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
+    st_volatile_u64(w, tag | (bits & 0xffffffffull));
+    st_volatile_u64(w + 1, tag | (bits >> 32));
 }
 
 // One warp.  Lane i < n (1 <= n <= kPeerRedMax) contributes v; returns the
@@ -157,17 +162,12 @@ __device__ __forceinline__ double peer_allreduce_warp(const PeerDev& pd, double 
     const int par = static_cast<int>(e & 1);
     const unsigned e32 = static_cast<unsigned>(e);
     const unsigned long long tag = static_cast<unsigned long long>(e32) << 32;
-    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
     if (lane < n)
-        for (int q = 0; q < pd.P; ++q) {
-            unsigned long long* w = pd.win[q]->red_ll[par][pd.rank][lane];
-            st_volatile_u64(w, tag | (bits & 0xffffffffull));
-            st_volatile_u64(w + 1, tag | (bits >> 32));
-        }
+        for (int q = 0; q < pd.P; ++q) peer_ll_store(pd.win[q]->red_ll[par][pd.rank][lane], v, tag);
     double t = 0.0;
     if (lane < n)
         for (int q = 0; q < pd.P; ++q)
-            t = add_rn(t, peer_ll_read(me->red_ll[par][q][lane], e32, me, q, e));
+            t = add_rn(t, peer_ll_read(me->red_ll[par][q][lane], e32, me, 2, q, e));
     __syncwarp();
     if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(&me->seq_r) = e;
     return t;
