@@ -96,6 +96,8 @@ static lbk_status ctx_create_impl(int device, void* stream, bool own, lbk_ctx* o
             ctx->l2_persist = (e && e[0] == '1') ? 1 : 0;
             if (ctx->l2_persist && ctx->persist_max)
                 cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(lim));
+            const char* pdl = std::getenv("LBK_PDL");
+            ctx->pdl = (pdl && pdl[0] == '0') ? 0 : 1;  // on unless LBK_PDL=0
         }
         {
             // solver workspaces come from the stream-ordered pool; keep freed

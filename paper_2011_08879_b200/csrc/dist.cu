@@ -286,6 +286,7 @@ struct PeerComm final : Comm {
 
 __global__ void peer_allreduce_kernel(PeerDev pd, double* dev, int count)
 {
+    pdl_enter();
     const int lane = threadIdx.x;
     const double v = lane < count ? dev[lane] : 0.0;
     const double t = peer_allreduce_warp(pd, v, count > 0 ? count : 1);
@@ -315,6 +316,7 @@ __device__ __forceinline__ int seg_of(const int* off, int P, int i)
 __global__ void peer_push_kernel(PeerDev pd, const int* __restrict__ send_off,
                                  const int* __restrict__ send_idx, const double* __restrict__ x)
 {
+    pdl_enter();
     __shared__ int so[kPeerMax + 1];
     PeerHdr* me = pd.win[pd.rank];
     const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&me->seq_x) + 1;
@@ -338,6 +340,7 @@ __global__ void peer_push_kernel(PeerDev pd, const int* __restrict__ send_off,
 __global__ void peer_recv_kernel(PeerDev pd, const int* __restrict__ recv_off,
                                  double* __restrict__ ghost)
 {
+    pdl_enter();
     __shared__ int ro[kPeerMax + 1];
     PeerHdr* me = pd.win[pd.rank];
     const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&me->seq_x) + 1;
@@ -439,15 +442,15 @@ void peer_push(lbk_ctx ctx, const lbk_dist_csr_s* D, const PeerDev& pd, const do
         need(D->send_off[q + 1] - D->send_off[q] <= pd.cap &&
                  D->recv_off[q + 1] - D->recv_off[q] <= pd.cap,
              LBK_USAGE_ERROR, "peer communicator: halo capacity too small for this matrix");
-    peer_push_kernel<<<peer_grid(D->send_off.back()), 256, 0, ctx->stream>>>(
-        pd, D->send_off_d.as<int>(), D->send_idx.as<int>(), x);
+    launch_pdl(ctx, peer_push_kernel, dim3(peer_grid(D->send_off.back())), dim3(256), 0, pd,
+               D->send_off_d.as<int>(), D->send_idx.as<int>(), x);
     LBK_LAUNCH_CHECK();
 }
 
 void peer_recv(lbk_ctx ctx, const lbk_dist_csr_s* D, const PeerDev& pd, double* ghost)
 {
-    peer_recv_kernel<<<peer_grid(D->recv_off.back()), 256, 0, ctx->stream>>>(
-        pd, D->recv_off_d.as<int>(), ghost);
+    launch_pdl(ctx, peer_recv_kernel, dim3(peer_grid(D->recv_off.back())), dim3(256), 0, pd,
+               D->recv_off_d.as<int>(), ghost);
     LBK_LAUNCH_CHECK();
 }
 

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "lbk.h"
 
@@ -65,6 +66,10 @@ struct lbk_ctx_s {
     // misses.  0 off, 1 on; persist_max = the device's window / carve-out.
     int l2_persist = 0;
     size_t persist_max = 0;
+    // programmatic dependent launch for the SpMV / solver kernel chain (on;
+    // LBK_PDL=0 turns it off): a kernel's CTAs are scheduled while its
+    // predecessor drains and wait in griddepcontrol.wait for its results
+    int pdl = 0;
 };
 
 namespace lbk {
@@ -266,6 +271,38 @@ __device__ __forceinline__ bool grid_reduce_finish(const double (&v)[NV], RedWs 
         *ws.counter = 0;
     }
     return true;
+}
+
+// First statement of every kernel that may be launched with programmatic
+// stream serialization: wait for the predecessor grid's completion (and
+// memory flush), then let the successor's CTAs be scheduled.  A no-op for
+// ordinary launches.
+__device__ __forceinline__ void pdl_enter()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(lbk_ctx ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                Args&&... args)
+{
+    if (!ctx->pdl) {
+        kernel<<<grid, block, smem, ctx->stream>>>(std::forward<Args>(args)...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...) != cudaSuccess)
+        throw std::runtime_error("kernel launch failed");
 }
 
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }

@@ -695,6 +695,7 @@ struct EpiGmApply {
 template <class Op>
 __global__ void __launch_bounds__(256) vec_kernel(long long n, Op op, RedWs ws)
 {
+    pdl_enter();
     constexpr int NV = Op::NV;
     __shared__ double sh[32 * NV];
     if (op.skip()) return;
@@ -1013,7 +1014,7 @@ void launch_vec(lbk_ctx ctx, long long n, const Op& op, RedWs ws)
     long long cap = static_cast<long long>(ctx->num_sms) * bps;
     if (cap > kRedMaxBlocks) cap = kRedMaxBlocks;
     int grid = static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap);
-    k<<<grid, 256, 0, ctx->stream>>>(n, op, ws);
+    launch_pdl(ctx, k, dim3(grid), dim3(256), 0, n, op, ws);
     LBK_LAUNCH_CHECK();
 }
 
@@ -1114,6 +1115,7 @@ __global__ void finish_kernel(E e, const double* tot)
 template <class E>
 __global__ void peer_finish_kernel(E e, const double* base, int has_a, int has_b, PeerDev pd)
 {
+    pdl_enter();
     if (e.skip()) return;
     static_assert(E::NV <= 8, "peer finish: at most 8 values");
     const int lane = threadIdx.x;
@@ -1155,7 +1157,8 @@ struct DistEnv {
     {
         // peer group: combine + the rank sum + finish() in one launch
         if (const PeerDev* pd = comm ? comm->peer() : nullptr) {
-            peer_finish_kernel<E><<<1, 32, 0, ctx->stream>>>(e, ws.out, has_a, has_b, *pd);
+            launch_pdl(ctx, peer_finish_kernel<E>, dim3(1), dim3(32), 0, e, ws.out, has_a, has_b,
+                       *pd);
             LBK_LAUNCH_CHECK();
             return;
         }

@@ -564,6 +564,7 @@ template <typename T, class Epi, int G>
 __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
     csr_stream_kernel(CsrView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
 {
+    pdl_enter();
     using Cfg = StreamCfg<T, 1>;
     constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -645,6 +646,7 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
     sellp_stream_kernel(SellpView<T> A, const int* __restrict__ tile_slices, int ntiles,
                         long long stored, const T* __restrict__ x, Epi epi, RedWs ws)
 {
+    pdl_enter();
     using Cfg = StreamCfg<T, 1>;
     using EP = EpiPre<Epi>;
     constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
@@ -750,6 +752,7 @@ template <typename T, class Epi, int G>
 __global__ void __launch_bounds__((StreamCfg<T, 2>::kThreads), 2)
     coo_stream_kernel(CooView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
 {
+    pdl_enter();
     using Cfg = StreamCfg<T, 2>;
     constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -880,6 +883,7 @@ __global__ void __launch_bounds__(256)
                        const int* __restrict__ cols, const T* __restrict__ vals,
                        const T* __restrict__ x, Epi epi, RedWs ws)
 {
+    pdl_enter();
     constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
     __shared__ double red_sh[32 * NV];
     if (epi.skip()) return;
@@ -957,6 +961,7 @@ __global__ void __launch_bounds__(256)
                        const int* __restrict__ cols, const T* __restrict__ vals,
                        const T* __restrict__ x, Epi epi, RedWs ws)
 {
+    pdl_enter();
     constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
     constexpr int U = 8;
     __shared__ double red_sh[32 * NV];
@@ -1014,6 +1019,7 @@ __global__ void __launch_bounds__(256)
                       const int* __restrict__ cols, const T* __restrict__ vals,
                       const T* __restrict__ x, Epi epi, RedWs ws)
 {
+    pdl_enter();
     constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
     __shared__ double red_sh[32 * NV];
     if (epi.skip()) return;

@@ -70,6 +70,7 @@ template <typename T, class Epi>
 __global__ void __launch_bounds__(256)
     csr_warp_kernel(CsrView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
 {
+    pdl_enter();
     constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
     __shared__ double red_sh[32 * NV];
     if (epi.skip()) return;
@@ -112,7 +113,8 @@ template <typename... KArgs, typename... Args>
 void launch_k(lbk_ctx ctx, void (*kernel)(KArgs...), int grid, int block, size_t smem,
               const void* x, size_t x_bytes, Args&&... args)
 {
-    if (!ctx->l2_persist || !x || !ctx->persist_max) {
+    const bool window = ctx->l2_persist && x && ctx->persist_max;
+    if (!window && !ctx->pdl) {
         kernel<<<grid, block, smem, ctx->stream>>>(std::forward<Args>(args)...);
         return;
     }
@@ -121,16 +123,25 @@ void launch_k(lbk_ctx ctx, void (*kernel)(KArgs...), int grid, int block, size_t
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    const size_t nb = x_bytes < ctx->persist_max ? x_bytes : ctx->persist_max;
-    attr[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(x);
-    attr[0].val.accessPolicyWindow.num_bytes = nb;
-    attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (window) {
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        const size_t nb = x_bytes < ctx->persist_max ? x_bytes : ctx->persist_max;
+        attr[na].val.accessPolicyWindow.base_ptr = const_cast<void*>(x);
+        attr[na].val.accessPolicyWindow.num_bytes = nb;
+        attr[na].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
+    }
+    if (ctx->pdl) {  // every kernel launched here opens with pdl_enter()
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     LBK_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
