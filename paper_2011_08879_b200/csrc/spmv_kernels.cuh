@@ -877,6 +877,9 @@ struct Quad<float> {
 // value loads, then 4 independent gathers.  Row sums keep the reference's
 // ascending-j order.  Requires: slice height % 4 == 0 and 16-B aligned
 // arrays (checked by the host).
+#ifndef LBK_QUAD_COLS
+#define LBK_QUAD_COLS 6
+#endif
 template <typename T, class Epi, bool IS_ELL>
 __global__ void __launch_bounds__(256)
     sliced_quad_kernel(int nrows, int S, const int* __restrict__ slice_sets, int ell_width,
@@ -910,6 +913,32 @@ __global__ void __launch_bounds__(256)
         }
         T sum[4] = {T(0), T(0), T(0), T(0)};
         int j = 0;
+        // U columns per step: 4U gathers per thread in flight
+        constexpr int U = LBK_QUAD_COLS;
+        for (; j + U - 1 < len; j += U) {
+            int cc[U][4];
+            Quad<T> vv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long o = base + (j + u) * pitch;
+                const int4 c = ld_stream_i4(cols + o);
+                cc[u][0] = c.x;
+                cc[u][1] = c.y;
+                cc[u][2] = c.z;
+                cc[u][3] = c.w;
+                vv[u].load(vals + o);
+            }
+            T g[U][4];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) g[u][i] = cc[u][i] >= 0 ? ldg_nc(x + cc[u][i]) : T(0);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (cc[u][i] >= 0) sum[i] = add_rn(sum[i], mul_rn(vv[u].v[i], g[u][i]));
+        }
         for (; j + 1 < len; j += 2) {
             const long long o0 = base + j * pitch, o1 = o0 + pitch;
             const int4 c0 = ld_stream_i4(cols + o0), c1 = ld_stream_i4(cols + o1);
