@@ -302,14 +302,6 @@ void PeerComm::allreduce_sum(double* dev, int count, cudaStream_t s)
     LBK_LAUNCH_CHECK();
 }
 
-// rank q of the (<= kPeerMax) segments [off[q], off[q+1]) holding entry i
-__device__ __forceinline__ int seg_of(const int* off, int P, int i)
-{
-    int q = 0;
-    while (q + 1 < P && i >= off[q + 1]) ++q;
-    return q;
-}
-
 // gather x[send_idx] and store each peer's run, LL-tagged with the halo
 // epoch, into its staging slot (parity e & 1, source = this rank) -- once
 // the receiver has handed back the slot's previous epoch
@@ -335,42 +327,6 @@ __global__ void peer_push_kernel(PeerDev pd, const int* __restrict__ send_off,
     }
 }
 
-// read the neighbours' tagged values of epoch e into the ghosts behind
-// x_local, hand the slots back, advance the halo epoch
-__global__ void peer_recv_kernel(PeerDev pd, const int* __restrict__ recv_off,
-                                 double* __restrict__ ghost)
-{
-    pdl_enter();
-    __shared__ int ro[kPeerMax + 1];
-    PeerHdr* me = pd.win[pd.rank];
-    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&me->seq_x) + 1;
-    const int par = static_cast<int>(e & 1);
-    if (threadIdx.x <= pd.P) ro[threadIdx.x] = recv_off[threadIdx.x];
-    __syncthreads();
-    const int nr = ro[pd.P];
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x) {
-        const int q = seg_of(ro, pd.P, i);
-        ghost[i] = peer_ll_read(pd.stage(pd.rank, par, q) + 2 * size_t(i - ro[q]),
-                                static_cast<unsigned>(e), me, 0, q, e);
-    }
-    // every value read has been consumed (stored) above: the slot may be
-    // overwritten as soon as the senders see the hand-back
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (atomicAdd(&me->recv_cnt, 1u) == gridDim.x - 1) {
-            me->recv_cnt = 0;
-            for (int q = 0; q < pd.P; ++q)
-                if (ro[q + 1] > ro[q]) st_volatile_u64(&pd.win[q]->empty[pd.rank], e);
-            *reinterpret_cast<volatile unsigned long long*>(&me->seq_x) = e;
-        }
-    }
-}
-
-int peer_grid(int n)
-{
-    const int b = ceil_div(n, 256);
-    return b < 1 ? 1 : (b > 296 ? 296 : b);
-}
 
 __global__ void pack_kernel(int n, const int* __restrict__ idx, const double* __restrict__ x,
                             double* __restrict__ out)
@@ -447,12 +403,6 @@ void peer_push(lbk_ctx ctx, const lbk_dist_csr_s* D, const PeerDev& pd, const do
     LBK_LAUNCH_CHECK();
 }
 
-void peer_recv(lbk_ctx ctx, const lbk_dist_csr_s* D, const PeerDev& pd, double* ghost)
-{
-    launch_pdl(ctx, peer_recv_kernel, dim3(peer_grid(D->recv_off.back())), dim3(256), 0, pd,
-               D->recv_off_d.as<int>(), ghost);
-    LBK_LAUNCH_CHECK();
-}
 
 }  // namespace lbk
 

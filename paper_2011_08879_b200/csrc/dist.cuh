@@ -175,9 +175,86 @@ namespace lbk {
 
 void dist_pack(lbk_ctx ctx, const lbk_dist_csr_s* D, const double* x);
 // peer-memory halo: gather + remote store into the neighbours' staging
-// slots, and (after the interior rows) wait + copy the staged ghosts
+// slots (before the interior rows)
 void peer_push(lbk_ctx ctx, const lbk_dist_csr_s* D, const PeerDev& pd, const double* x);
-void peer_recv(lbk_ctx ctx, const lbk_dist_csr_s* D, const PeerDev& pd, double* ghost);
+
+// Peer-memory boundary rows, fused with the halo receive: thread per
+// boundary row, summed sequentially in ascending k (the reference's bits
+// for every row length); a ghost column is read straight from this rank's
+// staging slot, spinning on its LL tag, so no separate receive kernel or
+// ghost copy runs.  Every block then counts itself out; the last one hands
+// the slots back and advances the halo epoch -- also when the solver is
+// done and the rows are skipped, so all ranks' epochs stay in step.
+template <class Epi>
+__global__ void __launch_bounds__(256)
+    peer_boundary_kernel(PeerDev pd, int nrows, const int* __restrict__ rp,
+                         const int* __restrict__ cols, const double* __restrict__ vals,
+                         const int* __restrict__ row_map, int row_off, int n_local,
+                         const int* __restrict__ recv_off, const double* __restrict__ x, Epi epi,
+                         RedWs ws)
+{
+    pdl_enter();
+    constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
+    __shared__ double red_sh[32 * NV];
+    __shared__ int ro[kPeerMax + 1];
+    PeerHdr* me = pd.win[pd.rank];
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&me->seq_x) + 1;
+    const int par = static_cast<int>(e & 1);
+    if (threadIdx.x <= pd.P) ro[threadIdx.x] = __ldg(recv_off + threadIdx.x);
+    __syncthreads();
+    const bool skip = epi.skip();
+    double acc[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    if (!skip) {
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows;
+             i += gridDim.x * blockDim.x) {
+            double s = 0.0;
+            const int kb = __ldg(rp + i), ke = __ldg(rp + i + 1);
+            for (int k = kb; k < ke; ++k) {
+                const int c = __ldg(cols + k);
+                double xv;
+                if (c < n_local) {
+                    xv = __ldg(x + c);
+                } else {
+                    const int g = c - n_local;
+                    const int q = seg_of(ro, pd.P, g);
+                    xv = peer_ll_read(pd.stage(pd.rank, par, q) + 2 * size_t(g - ro[q]),
+                                      static_cast<unsigned>(e), me, 0, q, e);
+                }
+                s = add_rn(s, mul_rn(__ldg(vals + k), xv));
+            }
+            epi.row(row_map ? __ldg(row_map + i) : i + row_off, s, acc);
+        }
+    }
+    // every ghost this block needed has been consumed: count out; the last
+    // block hands the slots back and advances the halo epoch
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&me->recv_cnt, 1u) == gridDim.x - 1) {
+        me->recv_cnt = 0;
+        for (int q = 0; q < pd.P; ++q)
+            if (ro[q + 1] > ro[q]) st_volatile_u64(&pd.win[q]->empty[pd.rank], e);
+        *reinterpret_cast<volatile unsigned long long*>(&me->seq_x) = e;
+    }
+    if constexpr (Epi::NV > 0) {
+        if (skip) return;
+        block_sum<NV>(acc, threadIdx.x, blockDim.x, red_sh);
+        grid_reduce_finish<NV>(acc, ws, threadIdx.x, blockDim.x, red_sh,
+                               [&](const double* tot) { epi.finish(tot); });
+    }
+}
+
+template <class Epi>
+void peer_boundary(lbk_ctx ctx, const lbk_dist_csr_s* D, const PeerDev& pd, const double* x,
+                   const Epi& epi, RedWs ws)
+{
+    const SubCsr& S = D->boundary;
+    launch_pdl(ctx, peer_boundary_kernel<Epi>, dim3(peer_grid(S.nrows)), dim3(256), 0, pd,
+               S.nrows, S.row_ptr.as<int>(), S.cols.as<int>(), S.vals.as<double>(),
+               S.row_off >= 0 ? nullptr : S.row_map.as<int>(), S.row_off >= 0 ? S.row_off : 0,
+               D->n_local, D->recv_off_d.as<int>(), x, epi, ws);
+    LBK_LAUNCH_CHECK();
+}
 
 // y = A x_ext with the halo exchange overlapped with the interior rows.
 // `epi` reduces over interior rows into ws_a.out and boundary rows into
@@ -191,8 +268,7 @@ void dist_apply(lbk_ctx ctx, lbk_dist_csr_s* D, Comm* comm, double* x_ext, const
         const PeerDev& pd = *comm->peer();
         peer_push(ctx, D, pd, x_ext);
         if (D->interior.nrows > 0) launch_sub(ctx, D->interior, x_ext, epi, ws_a);
-        peer_recv(ctx, D, pd, x_ext + D->n_local);
-        if (D->boundary.nrows > 0) launch_sub(ctx, D->boundary, x_ext, epi, ws_b);
+        peer_boundary(ctx, D, pd, x_ext, epi, ws_b);  // always: it advances the epoch
         return;
     }
     if (xchg) {

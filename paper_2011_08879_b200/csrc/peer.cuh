@@ -13,9 +13,9 @@
 //
 //   halo     the pack kernel gathers the values a peer needs and stores
 //            them, tagged, straight into that peer's staging slot; after
-//            the interior rows, the receive kernel waits for each word's
-//            tag, writes the ghosts behind x_local and hands the slot back
-//            (`empty` word in the sender's window).
+//            the interior rows, the boundary-row kernel (dist.cuh) reads
+//            each ghost from the slot as its tag arrives and hands the slot
+//            back (`empty` word in the sender's window).
 //   scalars  the finishing kernel of each fused reduction posts the rank's
 //            totals into every window's mailbox, waits for all P posts and
 //            sums them in rank order -- the same bits on every rank -- then
@@ -148,6 +148,20 @@ __device__ __forceinline__ void peer_ll_store(unsigned long long* w, double v,
     const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
     st_volatile_u64(w, tag | (bits & 0xffffffffull));
     st_volatile_u64(w + 1, tag | (bits >> 32));
+}
+
+// rank q of the (<= kPeerMax) segments [off[q], off[q+1]) holding entry i
+__device__ __forceinline__ int seg_of(const int* off, int P, int i)
+{
+    int q = 0;
+    while (q + 1 < P && i >= off[q + 1]) ++q;
+    return q;
+}
+
+inline int peer_grid(long long n)
+{
+    const long long b = (n + 255) / 256;
+    return b < 1 ? 1 : (b > 296 ? 296 : static_cast<int>(b));
 }
 
 // One warp.  Lane i < n (1 <= n <= kPeerRedMax) contributes v; returns the
