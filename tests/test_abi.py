@@ -73,6 +73,25 @@ def test_context_create_reports_cuda_error_without_device():
     assert b"" != lib.lbk_last_error(None)
 
 
+def test_peer_communicator_fails_loudly_without_device():
+    """The peer-memory communicator allocates its window on the device:
+    without one it reports a CUDA error (no host fallback); bad arguments
+    are usage errors before any device call."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    from paper_2011_08879_b200 import _lib as L
+    lib = L.load()
+    h = ctypes.c_void_p()
+    assert lib.lbk_comm_init_peer(2, 0, 0, 1024, ctypes.byref(h)) == L.CUDA_ERROR
+    assert lib.lbk_comm_init_peer(17, 0, 0, 1024, ctypes.byref(h)) == L.USAGE_ERROR
+    assert lib.lbk_comm_init_peer(2, 2, 0, 1024, ctypes.byref(h)) == L.USAGE_ERROR
+    assert lib.lbk_comm_peer_handle(None, None) == L.USAGE_ERROR
+    devs = (ctypes.c_int32 * 2)(0, 0)
+    arr = (ctypes.c_void_p * 2)()
+    assert lib.lbk_comm_init_peer_group(2, devs, 1024, arr) == L.USAGE_ERROR  # shared device
+
+
 def test_no_oracle_import_in_product():
     pkg = os.path.join(ROOT, "paper_2011_08879_b200")
     for dirpath, _, files in os.walk(pkg):
