@@ -35,8 +35,8 @@ void* scratch(lbk_ctx ctx, size_t bytes)
 
 RedWs red_ws(lbk_ctx ctx, int max_blocks, int slots)
 {
-    // Layout: [counter (256 B)] [out: 32 doubles] [partials]
-    const size_t need_bytes = 256 + 32 * sizeof(double) +
+    // Layout: [counter (256 B)] [out: 64 doubles] [partials]
+    const size_t need_bytes = 256 + 64 * sizeof(double) +
                               size_t(max_blocks) * slots * sizeof(double);
     if (ctx->red.bytes < need_bytes) {
         if (ctx->red.ptr) {
@@ -52,7 +52,7 @@ RedWs red_ws(lbk_ctx ctx, int max_blocks, int slots)
     RedWs ws;
     ws.counter = reinterpret_cast<unsigned*>(base);
     ws.out = reinterpret_cast<double*>(base + 256);
-    ws.partials = reinterpret_cast<double*>(base + 256 + 32 * sizeof(double));
+    ws.partials = reinterpret_cast<double*>(base + 256 + 64 * sizeof(double));
     return ws;
 }
 

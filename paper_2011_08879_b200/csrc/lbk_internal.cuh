@@ -81,7 +81,7 @@ void* scratch(lbk_ctx ctx, size_t bytes);
 struct RedWs {
     double* partials;     // [max_blocks * slots]
     unsigned* counter;    // zero between uses
-    double* out;          // [slots] device result
+    double* out;          // [64] device results (dist solver: see DistEnv)
     int defer = 0;        // 1: the finisher only stores the grid totals to
                           // `out` (a cross-rank allreduce runs before the
                           // epilogue's finish(), see dist.cu)

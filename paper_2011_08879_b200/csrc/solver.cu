@@ -1053,6 +1053,7 @@ const char* breakdown_what(int w)
 // launch (RedWs.defer = 0).
 template <class MatOp>
 struct LocalEnv {
+    static constexpr bool kMergeCg = false;
     lbk_ctx ctx;
     MatOp op;
     RedWs ws;
@@ -1131,7 +1132,63 @@ __global__ void peer_finish_kernel(E e, const double* base, int has_a, int has_b
     if (lane == 0) e.finish(tot);
 }
 
+// CG over the peer group with two exchanges per iteration instead of three:
+// K3's ||b - Ax||^2 stays rank-local (deferred to out[32], out[40]) and is
+// exchanged together with the next K1's <p, Ap>.  Its finish (history,
+// convergence) then runs here, before K1's -- the same totals, bits and
+// order of state updates as the three-exchange path; only the decision to
+// stop arrives one kernel later (K1's SpMV of that step is wasted work).
+template <class E1, class E3>
+__global__ void peer_finish_cg_kernel(E1 e1, E3 e3, const double* base, int has_a, int has_b,
+                                      PeerDev pd)
+{
+    pdl_enter();
+    if (e1.skip()) return;
+    const int lane = threadIdx.x;
+    const bool pending = e1.st->iter > 0;  // a K3 ran since the last K1
+    double v = 0.0;
+    if (lane == 0) {
+        if (has_a) v = add_rn(v, base[0]);
+        if (has_b) v = add_rn(v, base[8]);
+    } else if (lane == 1 && pending) {
+        if (has_a) v = add_rn(v, base[32]);
+        if (has_b) v = add_rn(v, base[40]);
+    }
+    const double t = peer_allreduce_warp(pd, v, 2);
+    __shared__ double tot[2];
+    if (lane < 2) tot[lane] = t;
+    __syncwarp();
+    if (lane == 0) {
+        if (pending) {
+            e3.finish(&tot[1]);
+            if (e1.st->done) return;
+        }
+        e1.finish(&tot[0]);
+    }
+}
+
+// the last K3's deferred residual, when the launch loop ends on it
+template <class E3>
+__global__ void peer_flush_cg_kernel(E3 e3, const double* base, int has_a, int has_b, PeerDev pd)
+{
+    pdl_enter();
+    if (e3.skip()) return;
+    const int lane = threadIdx.x;
+    double v = 0.0;
+    if (lane == 0) {
+        if (has_a) v = add_rn(v, base[32]);
+        if (has_b) v = add_rn(v, base[40]);
+    }
+    const double t = peer_allreduce_warp(pd, v, 1);
+    __shared__ double tot[1];
+    if (lane == 0) {
+        tot[0] = t;
+        e3.finish(tot);
+    }
+}
+
 struct DistEnv {
+    static constexpr bool kMergeCg = true;
     lbk_ctx ctx;
     lbk_dist_csr_s* D;
     Comm* comm;
@@ -1176,6 +1233,39 @@ struct DistEnv {
         wb.out = ws.out + 8;
         dist_apply(ctx, D, comm, x, e, wa, wb);
         finish(e, D->interior.nrows > 0, D->boundary.nrows > 0);
+    }
+    // two-exchange CG (peer group; LBK_CG_MERGE=0 turns it off)
+    bool merge_cg() const
+    {
+        const char* e = std::getenv("LBK_CG_MERGE");
+        return comm && comm->peer() && !(e && e[0] == '0');
+    }
+    template <class E1, class E3>
+    void apply_k1_merged(double* x, const E1& e1, const E3& e3)
+    {
+        RedWs wa = ws, wb = ws;
+        wa.defer = wb.defer = 1;
+        wb.out = ws.out + 8;
+        dist_apply(ctx, D, comm, x, e1, wa, wb);
+        launch_pdl(ctx, peer_finish_cg_kernel<E1, E3>, dim3(1), dim3(32), 0, e1, e3, ws.out,
+                   D->interior.nrows > 0 ? 1 : 0, D->boundary.nrows > 0 ? 1 : 0, *comm->peer());
+        LBK_LAUNCH_CHECK();
+    }
+    template <class E3>
+    void apply_k3_deferred(double* x, const E3& e3)
+    {
+        RedWs wa = ws, wb = ws;
+        wa.defer = wb.defer = 1;
+        wa.out = ws.out + 32;
+        wb.out = ws.out + 40;
+        dist_apply(ctx, D, comm, x, e3, wa, wb);
+    }
+    template <class E3>
+    void flush_k3(const E3& e3)
+    {
+        launch_pdl(ctx, peer_flush_cg_kernel<E3>, dim3(1), dim3(32), 0, e3, ws.out,
+                   D->interior.nrows > 0 ? 1 : 0, D->boundary.nrows > 0 ? 1 : 0, *comm->peer());
+        LBK_LAUNCH_CHECK();
     }
     template <class Op>
     void vec(const Op& o)
@@ -1371,6 +1461,8 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
 
     env.apply(x, EpiInit{b, r, p, rt, st, (bicg || cgs) ? 1 : 0, u});
 
+    bool merge = false;
+    if constexpr (Env::kMergeCg) merge = !bicg && !cgs && !recurrence && env.merge_cg();
     auto iteration = [&] {
         if (cgs) {
             // v and t share storage: v is dead once S3 has formed q, w
@@ -1380,6 +1472,14 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
             env.apply(w, EpiCgsT{t, x, r, w, rt, st});
             env.apply(x, EpiCgsRes{b, st});
         } else if (!bicg) {
+            if constexpr (Env::kMergeCg) {
+                if (merge && !recurrence) {
+                    env.apply_k1_merged(p, EpiCgK1{q, p, st}, EpiCgK3{b, p, r, st});
+                    env.vec(OpCgK2{x, r, p, q, st, 0, 0.0});
+                    env.apply_k3_deferred(x, EpiCgK3{b, p, r, st});
+                    return;
+                }
+            }
             env.apply(p, EpiCgK1{q, p, st});
             env.vec(OpCgK2{x, r, p, q, st, recurrence ? 1 : 0, 0.0});
             if (!recurrence) {
@@ -1446,6 +1546,9 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
         if (*done_host || launched >= limit) break;
     }
     if (gexec) cudaGraphExecDestroy(gexec);
+    if constexpr (Env::kMergeCg) {
+        if (merge) env.flush_k3(EpiCgK3{b, p, r, st});  // the launch loop ends on a K3
+    }
     finish_solve(ctx, env, st, hist, x, x_user, n, limit, cfg, res, history, hist_cap, ev0, ev1);
 }
 

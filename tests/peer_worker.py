@@ -40,7 +40,7 @@ def solve(kind, A, b, **kw):
     M, comm, lo, hi = setup(A)
     x = torch.zeros(hi - lo, dtype=torch.float64, device="cuda")
     cfg = lk.SolverConfig(kind=kind, rel_tol=kw.get("tol", 1e-8), max_iters=20000,
-                          gmres_restart=20)
+                          gmres_restart=20, fixed_iters=kw.get("fixed", 0))
     r = M.solve(comm, torch.from_numpy(b[lo:hi].copy()).cuda(), x, cfg)
     return {"iters": r.iterations, "hist": r.residual_history, "conv": r.converged,
             "flops": r.flop_count, "x": x.cpu().numpy().tolist()}
@@ -78,6 +78,10 @@ def main():
     # solvers
     A = O.stencil("7pt", 32)
     out["cg"] = solve("cg", A, O.spmv_csr(A, np.ones(A.nrows)))
+    os.environ["LBK_CG_MERGE"] = "0"  # three exchanges per iteration
+    out["cg_3x"] = solve("cg", A, O.spmv_csr(A, np.ones(A.nrows)))
+    os.environ.pop("LBK_CG_MERGE")
+    out["cg_fixed"] = solve("cg", A, O.spmv_csr(A, np.ones(A.nrows)), fixed=50)
     A = O.stencil("7pt", 20, 0.5)
     b = O.spmv_csr(A, O.seeded_values(A.nrows, 11))
     out["bicgstab"] = solve("bicgstab", A, b)

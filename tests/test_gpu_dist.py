@@ -230,6 +230,12 @@ def test_peer_solvers(peer_run, O):
             assert o[kind]["iters"] == r0["iters"] and o[kind]["hist"] == r0["hist"], kind
         assert r0["conv"], kind
     assert abs(out[0]["cg"]["iters"] - 81) <= 1  # golden
+    # two exchanges per CG iteration (K3's residual rides with the next
+    # <p,Ap>) give exactly the three-exchange path's history and x
+    assert out[0]["cg"]["hist"] == out[0]["cg_3x"]["hist"]
+    assert out[0]["cg"]["x"] == out[0]["cg_3x"]["x"]
+    # fixed iteration count: the loop ends on a deferred residual (flush)
+    assert out[0]["cg_fixed"]["iters"] == 50 and len(out[0]["cg_fixed"]["hist"]) == 51
     A = O.stencil("7pt", 32)
     I = out[0]["cg"]["iters"]
     assert out[0]["cg"]["flops"] == I * (4 * A.nnz + 16 * A.nrows) + 2 * A.nnz + 4 * A.nrows
