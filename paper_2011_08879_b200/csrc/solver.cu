@@ -60,7 +60,7 @@ struct SolverState {
     int limit;
     int fixed;
     int verify_pending;  // residual_mode 1: true residual requested
-    int pad;
+    int res_pending;     // peer two-exchange path: a deferred residual awaits
     double tol, norm_b;
     double rho, rho_next, alpha, beta, omega;
     double s_rel;
@@ -1132,12 +1132,13 @@ __global__ void peer_finish_kernel(E e, const double* base, int has_a, int has_b
     if (lane == 0) e.finish(tot);
 }
 
-// CG over the peer group with two exchanges per iteration instead of three:
-// K3's ||b - Ax||^2 stays rank-local (deferred to out[32], out[40]) and is
-// exchanged together with the next K1's <p, Ap>.  Its finish (history,
-// convergence) then runs here, before K1's -- the same totals, bits and
-// order of state updates as the three-exchange path; only the decision to
-// stop arrives one kernel later (K1's SpMV of that step is wasted work).
+// CG / BiCGSTAB over the peer group with one exchange fewer per iteration:
+// the true residual ||b - Ax||^2 of K3 (CG) / B6 (BiCGSTAB) stays
+// rank-local (deferred to out[32], out[40]) and is exchanged together with
+// the next K1's <p, Ap> / B2's <rt, v>.  Its finish (history, convergence)
+// then runs here, before K1's -- the same totals, bits and order of state
+// updates as the unmerged path; only the decision to stop arrives one
+// kernel later (that K1's SpMV is wasted work).
 template <class E1, class E3>
 __global__ void peer_finish_cg_kernel(E1 e1, E3 e3, const double* base, int has_a, int has_b,
                                       PeerDev pd)
@@ -1145,7 +1146,7 @@ __global__ void peer_finish_cg_kernel(E1 e1, E3 e3, const double* base, int has_
     pdl_enter();
     if (e1.skip()) return;
     const int lane = threadIdx.x;
-    const bool pending = e1.st->iter > 0;  // a K3 ran since the last K1
+    const bool pending = e1.st->res_pending != 0;  // a K3 ran since the last K1
     double v = 0.0;
     if (lane == 0) {
         if (has_a) v = add_rn(v, base[0]);
@@ -1164,6 +1165,7 @@ __global__ void peer_finish_cg_kernel(E1 e1, E3 e3, const double* base, int has_
             if (e1.st->done) return;
         }
         e1.finish(&tot[0]);
+        e1.st->res_pending = 1;  // this iteration's K3 follows, deferred
     }
 }
 
@@ -1172,7 +1174,7 @@ template <class E3>
 __global__ void peer_flush_cg_kernel(E3 e3, const double* base, int has_a, int has_b, PeerDev pd)
 {
     pdl_enter();
-    if (e3.skip()) return;
+    if (e3.skip() || !e3.st->res_pending) return;
     const int lane = threadIdx.x;
     double v = 0.0;
     if (lane == 0) {
@@ -1462,7 +1464,7 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
     env.apply(x, EpiInit{b, r, p, rt, st, (bicg || cgs) ? 1 : 0, u});
 
     bool merge = false;
-    if constexpr (Env::kMergeCg) merge = !bicg && !cgs && !recurrence && env.merge_cg();
+    if constexpr (Env::kMergeCg) merge = !cgs && !gmres && !recurrence && env.merge_cg();
     auto iteration = [&] {
         if (cgs) {
             // v and t share storage: v is dead once S3 has formed q, w
@@ -1489,6 +1491,16 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
                 env.vec(OpCgP{p, r, st, 0.0});
             }
         } else {
+            if constexpr (Env::kMergeCg) {
+                if (merge) {
+                    env.apply_k1_merged(p, EpiBiB2{q, rt, st}, EpiBiB6{b, p, q, r, st});
+                    env.vec(OpBiB3{s, r, q, st, 0.0});
+                    env.apply(s, EpiBiB4{t, s, st});
+                    env.vec(OpBiB5{x, r, p, s, t, rt, st, 0.0, 0.0});
+                    env.apply_k3_deferred(x, EpiBiB6{b, p, q, r, st});
+                    return;
+                }
+            }
             env.apply(p, EpiBiB2{q, rt, st});
             env.vec(OpBiB3{s, r, q, st, 0.0});
             env.apply(s, EpiBiB4{t, s, st});
@@ -1547,7 +1559,9 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
     }
     if (gexec) cudaGraphExecDestroy(gexec);
     if constexpr (Env::kMergeCg) {
-        if (merge) env.flush_k3(EpiCgK3{b, p, r, st});  // the launch loop ends on a K3
+        // the launch loop ends on a deferred residual
+        if (merge && bicg) env.flush_k3(EpiBiB6{b, p, q, r, st});
+        if (merge && !bicg) env.flush_k3(EpiCgK3{b, p, r, st});
     }
     finish_solve(ctx, env, st, hist, x, x_user, n, limit, cfg, res, history, hist_cap, ev0, ev1);
 }

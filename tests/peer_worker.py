@@ -88,6 +88,10 @@ def main():
     os.environ["LBK_SOLVER_GRAPH"] = "0"
     out["bicgstab_eager"] = solve("bicgstab", A, b)
     os.environ.pop("LBK_SOLVER_GRAPH")
+    os.environ["LBK_CG_MERGE"] = "0"  # the residual exchanged on its own
+    out["bicgstab_unmerged"] = solve("bicgstab", A, b)
+    os.environ.pop("LBK_CG_MERGE")
+    out["bicgstab_fixed"] = solve("bicgstab", A, b, fixed=23)
     A = O.stencil("7pt", 14, 0.5)
     b = O.spmv_csr(A, O.seeded_values(A.nrows, 11))
     out["cgs"] = solve("cgs", A, b)

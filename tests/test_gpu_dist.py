@@ -243,6 +243,10 @@ def test_peer_solvers(peer_run, O):
     assert np.max(np.abs(x - 1.0)) < 1e-5
     # captured graph and eager launches give the same bits
     assert out[0]["bicgstab"]["hist"] == out[0]["bicgstab_eager"]["hist"]
+    assert out[0]["bicgstab"]["hist"] == out[0]["bicgstab_unmerged"]["hist"]
+    assert out[0]["bicgstab"]["x"] == out[0]["bicgstab_unmerged"]["x"]
+    assert out[0]["bicgstab_fixed"]["iters"] == 23
+    assert len(out[0]["bicgstab_fixed"]["hist"]) == 24
     A = O.stencil("7pt", 20, 0.5)
     b = O.spmv_csr(A, O.seeded_values(A.nrows, 11))
     x = np.concatenate([o["bicgstab"]["x"] for o in out])
