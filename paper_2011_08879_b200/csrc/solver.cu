@@ -34,6 +34,7 @@
 // and must pass before convergence is declared.
 #include <chrono>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "api_guard.h"
@@ -850,6 +851,8 @@ struct OpCgsUP {
         u[i] = ui;
         p[i] = add_rn(mul_rn(add_rn(mul_rn(p[i], beta), qi), beta), ui);
     }
+    // nothing to reduce: the distributed path skips the rank exchange
+    static constexpr bool kNoFinish = true;
     __device__ void finish(const double*) const {}
 };
 
@@ -1189,6 +1192,13 @@ __global__ void peer_flush_cg_kernel(E3 e3, const double* base, int has_a, int h
     }
 }
 
+template <class Op, class = void>
+struct NoFinish : std::false_type {
+};
+template <class Op>
+struct NoFinish<Op, std::void_t<decltype(Op::kNoFinish)>> : std::bool_constant<Op::kNoFinish> {
+};
+
 struct DistEnv {
     static constexpr bool kMergeCg = true;
     lbk_ctx ctx;
@@ -1275,7 +1285,7 @@ struct DistEnv {
         RedWs wa = ws;
         wa.defer = 1;
         launch_vec(ctx, D->n_local, o, wa);
-        finish(o, 1, 0);
+        if constexpr (!NoFinish<Op>::value) finish(o, 1, 0);
     }
     void sync()
     {
