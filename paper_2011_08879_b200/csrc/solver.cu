@@ -768,6 +768,7 @@ struct OpCgP {
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     __device__ void prologue() { beta = st->beta; }
     __device__ void elem(long long i, double*) const { p[i] = add_rn(mul_rn(p[i], beta), r[i]); }
+    static constexpr bool kNoFinish = true;  // nothing to reduce
     __device__ void finish(const double*) const {}
 };
 
@@ -874,6 +875,7 @@ struct OpCgsQW {
         q[i] = qi;
         w[i] = add_rn(ui, qi);
     }
+    static constexpr bool kNoFinish = true;  // nothing to reduce
     __device__ void finish(const double*) const {}
 };
 
@@ -948,6 +950,7 @@ struct OpGmScale {
     __device__ bool skip() const { return gm_step_skip(st, jj); }
     __device__ void prologue() { inv = 1.0 / (w ? st->gm->hnext : st->gm->beta); }
     __device__ void elem(long long k, double*) const { v[k] = mul_rn(w ? w[k] : v[k], inv); }
+    static constexpr bool kNoFinish = true;  // nothing to reduce
     __device__ void finish(const double*) const {}
 };
 
