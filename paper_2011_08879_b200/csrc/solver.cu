@@ -693,6 +693,15 @@ struct EpiGmApply {
 };
 
 // ------------------------------------------------ element-wise steps
+// Ops that reduce nothing declare `static constexpr bool kNoFinish = true`:
+// no grid reduction, and no rank exchange on the distributed path.
+template <class Op, class = void>
+struct NoFinish : std::false_type {
+};
+template <class Op>
+struct NoFinish<Op, std::void_t<decltype(Op::kNoFinish)>> : std::bool_constant<Op::kNoFinish> {
+};
+
 template <class Op>
 __global__ void __launch_bounds__(256) vec_kernel(long long n, Op op, RedWs ws)
 {
@@ -707,9 +716,11 @@ __global__ void __launch_bounds__(256) vec_kernel(long long n, Op op, RedWs ws)
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         op.elem(i, acc);
-    block_sum<NV>(acc, threadIdx.x, blockDim.x, sh);
-    grid_reduce_finish<NV>(acc, ws, threadIdx.x, blockDim.x, sh,
-                           [&](const double* tot) { op.finish(tot); });
+    if constexpr (!NoFinish<Op>::value) {
+        block_sum<NV>(acc, threadIdx.x, blockDim.x, sh);
+        grid_reduce_finish<NV>(acc, ws, threadIdx.x, blockDim.x, sh,
+                               [&](const double* tot) { op.finish(tot); });
+    }
 }
 
 // CG K2: x += alpha p; r -= alpha q; <r,r>; beta = <r,r>/rho (for K3).
@@ -1194,13 +1205,6 @@ __global__ void peer_flush_cg_kernel(E3 e3, const double* base, int has_a, int h
         e3.finish(tot);
     }
 }
-
-template <class Op, class = void>
-struct NoFinish : std::false_type {
-};
-template <class Op>
-struct NoFinish<Op, std::void_t<decltype(Op::kNoFinish)>> : std::bool_constant<Op::kNoFinish> {
-};
 
 struct DistEnv {
     static constexpr bool kMergeCg = true;
