@@ -243,8 +243,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     ex_in = lk.CudaExecutor(local_rank, stream=s_in)
     ex_out = lk.CudaExecutor(local_rank, stream=s_out)
     ex_mv = lk.CudaExecutor(local_rank, stream=s_mv)
-    xb = [x.values, torch.empty_like(x.values)]
-    yb = [y.values, torch.empty_like(y.values)]
+    NB = int(os.environ.get("LBK_E2E_BUFFERS", "2"))  # device buffers in flight (3, 4: no gain)
+    xb = [x.values] + [torch.empty_like(x.values) for _ in range(NB - 1)]
+    yb = [y.values] + [torch.empty_like(y.values) for _ in range(NB - 1)]
     descs = desc
 
     def run_pipe(e0):
@@ -254,15 +255,15 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         mv_done = [torch.cuda.Event() for _ in range(K)]
         dn_done = [torch.cuda.Event() for _ in range(K)]
         for i in range(K):
-            j = i & 1
-            if i >= 2:
-                s_in.wait_event(mv_done[i - 2])  # x buffer j free again
+            j = i % NB
+            if i >= NB:
+                s_in.wait_event(mv_done[i - NB])  # x buffer j free again
             lk._check(lib.lbk_memcpy_h2d(ex_in.ctx, C.c_void_p(xb[j].data_ptr()), xhp, 8 * ncols),
                       ex_in.ctx)
             up_done[i].record(s_in)
             s_mv.wait_event(up_done[i])
-            if i >= 2:
-                s_mv.wait_event(dn_done[i - 2])  # y buffer j drained
+            if i >= NB:
+                s_mv.wait_event(dn_done[i - NB])  # y buffer j drained
             st = lib.lbk_spmv_csr_f64(ex_mv.ctx, C.byref(descs), C.c_void_p(xb[j].data_ptr()),
                                       C.c_void_p(yb[j].data_ptr()))
             if st:
