@@ -128,8 +128,12 @@ def _gloo_worker(rank, world, port, q):
         import torch
         t = torch.tensor([float(np.dot(y, y))], dtype=torch.float64)
         dist.all_reduce(t)
+        # the peer communicator's slot size: max over ranks of the largest
+        # per-peer halo (both directions); 7-pt 12^3 split in two: one plane
+        cap = D.peer_halo_cap(m)
         q.put((rank, bool(np.array_equal(y, yref)), float(t.item()), float(np.dot(O.spmv_csr(A, x),
-                                                                                  O.spmv_csr(A, x)))))
+                                                                                  O.spmv_csr(A, x))),
+               cap, m.halo_count()))
     finally:
         dist.destroy_process_group()
 
@@ -145,6 +149,7 @@ def test_gloo_world2_halo_protocol():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, ok, tot, ref in res:
+    for rank, ok, tot, ref, cap, mine in res:
         assert ok, rank
         assert abs(tot - ref) <= 1e-12 * ref
+        assert cap == 12 * 12 and mine == 12 * 12  # one 12x12 plane each way
