@@ -191,8 +191,12 @@ lbk_status lbk_sellp_plan(lbk_ctx, const lbk_sellp* A, int32_t* tile_slices_dev)
 lbk_status lbk_coo_plan(lbk_ctx, const lbk_coo* A, int32_t* tile_starts_dev);
 
 /* ------------------------------------------------------------ BLAS-1 */
-/* kernels.hpp:79-91, api.cpp:69-110.  Reductions are deterministic (fixed
- * two-stage tree), so repeated calls are bitwise reproducible. */
+/* kernels.hpp:79-91, api.cpp:69-110.  Reductions are exactly rounded:
+ * dot = RNE(sum_i RN(x_i y_i)), accumulated as integers (csrc/xred.cuh),
+ * so the result depends on neither the launch configuration nor, in the
+ * distributed solver, the partition -- bitwise reproducible everywhere
+ * (the reference's sequential and chunked sums, reference.cpp:46-56 /
+ * parallel.cpp:76-97, are two roundings of the same exact value). */
 lbk_status lbk_axpy_f64(lbk_ctx, int64_t n, double alpha, const double* x, double* y);
 lbk_status lbk_scal_f64(lbk_ctx, int64_t n, double alpha, double* x);
 lbk_status lbk_fill_f64(lbk_ctx, int64_t n, double value, double* x);
@@ -209,6 +213,17 @@ lbk_status lbk_dot_f64_dev(lbk_ctx, int64_t n, const double* x, const double* y,
 lbk_status lbk_stream_copy_f64(lbk_ctx, int64_t n, const double* a, double* c);
 lbk_status lbk_stream_triad_f64(lbk_ctx, int64_t n, double scalar, const double* b,
                                 const double* c, double* a);
+/* the rest of the reference's StreamOp set (kernels.hpp:58-68,
+ * reference.cpp:104-120): b <- s c (16 n bytes), c <- a + b (24 n bytes),
+ * sum a_i b_i to HOST (16 n bytes; exactly rounded, synchronises). */
+lbk_status lbk_stream_mul_f64(lbk_ctx, int64_t n, double scalar, const double* c, double* b);
+lbk_status lbk_stream_add_f64(lbk_ctx, int64_t n, const double* a, const double* b, double* c);
+lbk_status lbk_stream_dot_f64(lbk_ctx, int64_t n, const double* a, const double* b,
+                              double* result);
+/* flops_sweep (kernels.hpp:70-73, reference.cpp:124-130, fma_chain.hpp):
+ * x_i <- fma_chain(x_i, fma_per_element), bit-identical to the reference
+ * (2 flops per step, 16 n bytes per call). */
+lbk_status lbk_flops_sweep_f64(lbk_ctx, int64_t n, int32_t fma_per_element, double* x);
 
 /* ------------------------------------------------------- conversions */
 /* coo_to_csr (formats.cpp:132-155): row histogram + scan; col/vals are

@@ -76,6 +76,11 @@ def port():
             "port_part_ghosts": (i64, [C.c_int32, C.c_int32, C.c_int32, i32p, i32p, C.c_void_p, i64]),
             "port_part_local_cols": (None, [C.c_int32, C.c_int32, C.c_int32, i32p, i32p, i32p, i64, i32p]),
             "port_dot": (C.c_double, [i64, f64p, f64p]),
+            "port_xdot": (C.c_double, [i64, f64p, f64p]),
+            "port_xsum": (C.c_double, [i64, f64p]),
+            "port_xsolve": (C.c_int, [C.c_int, C.c_int32, i32p, i32p, f64p, f64p, f64p, C.c_double,
+                                      C.c_int, C.c_int, f64p, i64, C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int), C.POINTER(i64), C.POINTER(C.c_int)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -378,3 +383,34 @@ def ref_solve(a: Csr, b: np.ndarray, kind: str = "cg", x0=None, max_iters=1000,
                          max_iters, rel_tol, fixed_iters, restart, hist, cap, oi, od, C.byref(fl)))
     return RefSolve(bool(oi[0]), int(oi[1]), float(od[0]), hist[: oi[2]].copy(), fl.value,
                     float(od[1]), x)
+
+
+# ------------------------------------------------- exactly rounded reductions
+def xdot(x: np.ndarray, y: np.ndarray) -> float:
+    """RNE(sum RN(x_i y_i)) -- the product's partition-independent dot."""
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    return port().port_xdot(x.size, x, y)
+
+
+def xsum(v: np.ndarray) -> float:
+    v = np.ascontiguousarray(v, np.float64)
+    return port().port_xsum(v.size, v)
+
+
+def xsolve(a: Csr, b: np.ndarray, kind: str = "cg", x0=None, tol: float = 1e-8,
+           max_iters: int = 1000, fixed_iters: int = 0) -> dict:
+    """krylov.cpp CG / BiCGSTAB with exactly rounded dots (oracle/xkrylov.cpp)."""
+    k = {"cg": 0, "bicgstab": 1}[kind]
+    x = np.zeros(a.nrows) if x0 is None else np.array(x0, np.float64)
+    cap = (fixed_iters or max_iters) + 2
+    hist = np.zeros(cap)
+    it, conv, bd = C.c_int(), C.c_int(), C.c_int()
+    fl = i64(0)
+    st = port().port_xsolve(k, a.nrows, a.row_ptr, a.cols, a.vals,
+                            np.ascontiguousarray(b, np.float64), x, tol, max_iters,
+                            fixed_iters, hist, cap, C.byref(it), C.byref(conv), C.byref(fl),
+                            C.byref(bd))
+    return {"status": st, "iterations": it.value, "converged": bool(conv.value),
+            "history": hist[: it.value + 1].copy(), "flops": fl.value,
+            "breakdown_iter": bd.value, "x": x}

@@ -88,6 +88,17 @@ void port_part_local_cols(int32_t n, int32_t nparts, int32_t rank,
 /* ---- BLAS-1 (reference order: sequential) ---- */
 double port_dot(int64_t n, const double* x, const double* y);
 
+/* ---- exactly rounded reductions (oracle/xkrylov.cpp) ----
+ * RNE(sum of RN(x_i*y_i)): the product's partition-independent reduction. */
+double port_xdot(int64_t n, const double* x, const double* y);
+double port_xsum(int64_t n, const double* v);
+/* krylov.cpp CG (kind 0) / BiCGSTAB (kind 1) with exactly rounded dots.
+ * Returns 0, or 3 on BreakdownError (iteration in *bd_iter). */
+int port_xsolve(int kind, int32_t n, const int32_t* rp, const int32_t* ci, const double* vals,
+                const double* b, double* x, double tol, int max_iters, int fixed_iters,
+                double* hist_out, int64_t hist_cap, int* iterations, int* converged,
+                int64_t* flops, int* bd_iter);
+
 #ifdef __cplusplus
 }
 #endif

@@ -134,6 +134,10 @@ SIGNATURES = {
     "lbk_dot_f64_dev": (st, [vp, i64, vp, vp, vp]),
     "lbk_stream_copy_f64": (st, [vp, i64, vp, vp]),
     "lbk_stream_triad_f64": (st, [vp, i64, f64, vp, vp, vp]),
+    "lbk_stream_mul_f64": (st, [vp, i64, f64, vp, vp]),
+    "lbk_stream_add_f64": (st, [vp, i64, vp, vp, vp]),
+    "lbk_stream_dot_f64": (st, [vp, i64, vp, vp, P(f64)]),
+    "lbk_flops_sweep_f64": (st, [vp, i64, i32, vp]),
     "lbk_coo_to_csr": (st, [vp, P(lbk_coo), vp]),
     "lbk_csr_to_coo": (st, [vp, P(lbk_csr), vp]),
     "lbk_coo_assemble_f64": (st, [vp, i32, i32, i64, vp, vp, vp, vp, vp, vp, P(i64)]),

@@ -5,6 +5,7 @@
 // two-stage tree (per-block partials summed in block order by the last
 // block), so results are reproducible run to run; the order differs from
 // the reference's sequential sum (tolerance 1e-12, SPEC.md kernels module).
+#include <initializer_list>
 #include "api_guard.h"
 
 namespace lbk {
@@ -47,12 +48,13 @@ __global__ void dot_kernel(long long n, const double* __restrict__ x,
                            const double* __restrict__ y, RedWs ws, int take_sqrt)
 {
     __shared__ double sh[32];
-    double acc[1] = {0.0};
+    red_begin<1>();
+    RAcc acc[1];
+    racc_zero(acc[0]);
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
-        acc[0] = add_rn(acc[0], mul_rn(x[i], y[i]));
-    block_sum<1>(acc, threadIdx.x, blockDim.x, sh);
-    grid_reduce_finish<1>(acc, ws, threadIdx.x, blockDim.x, sh, [&](const double* t) {
+        racc_add(acc, 0, mul_rn(x[i], y[i]));
+    grid_reduce<1>(acc, ws, threadIdx.x, blockDim.x, sh, [&](const double* t) {
         ws.out[0] = take_sqrt ? sqrt(t[0]) : t[0];
     });
 }
@@ -104,6 +106,51 @@ __global__ void __launch_bounds__(256) stream_triad_kernel(long long n2, double 
          i += (long long)gridDim.x * blockDim.x) {
         const double2 x = __ldcs(b + i), y = __ldcs(c + i);
         __stcs(a + i, make_double2(add_rn(x.x, mul_rn(s, y.x)), add_rn(x.y, mul_rn(s, y.y))));
+    }
+}
+
+// stream mul b <- s c, add c <- a + b (reference.cpp:104-111)
+__global__ void __launch_bounds__(256) stream_mul_kernel(long long n2, double s,
+                                                         const double2* __restrict__ c,
+                                                         double2* __restrict__ b)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double2 y = __ldcs(c + i);
+        __stcs(b + i, make_double2(mul_rn(s, y.x), mul_rn(s, y.y)));
+    }
+}
+
+__global__ void __launch_bounds__(256) stream_add_kernel(long long n2,
+                                                         const double2* __restrict__ a,
+                                                         const double2* __restrict__ b,
+                                                         double2* __restrict__ c)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double2 x = __ldcs(a + i), y = __ldcs(b + i);
+        __stcs(c + i, make_double2(add_rn(x.x, y.x), add_rn(x.y, y.y)));
+    }
+}
+
+// flops sweep (reference.cpp:124-130 + fma_chain.hpp:14-21): x_i <- the
+// chain v = a_k v + 3 with a_k = 2, 0.5, 2, ... applied `count` times.
+// a_k is a power of two, so a_k v is exact and one FMA rounds exactly like
+// the reference's separate multiply and add: bit-identical, one DFMA/step.
+__global__ void __launch_bounds__(256) flops_sweep_kernel(long long n, int count,
+                                                          double* __restrict__ x)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double v = x[i];
+        int k = 0;
+#pragma unroll 8
+        for (; k + 1 < count; k += 2) {
+            v = fma(2.0, v, 3.0);
+            v = fma(0.5, v, 3.0);
+        }
+        if (k < count) v = fma(2.0, v, 3.0);
+        x[i] = v;
     }
 }
 
@@ -200,6 +247,61 @@ lbk_status lbk_stream_triad_f64(lbk_ctx ctx, int64_t n, double scalar, const dou
         stream_triad_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
             n / 2, scalar, reinterpret_cast<const double2*>(b), reinterpret_cast<const double2*>(c),
             reinterpret_cast<double2*>(a));
+        LBK_LAUNCH_CHECK();
+    });
+}
+
+static bool pair_aligned(int64_t n, std::initializer_list<const void*> ps)
+{
+    if (n % 2) return false;
+    for (const void* p : ps)
+        if (reinterpret_cast<uintptr_t>(p) & 15) return false;
+    return true;
+}
+
+lbk_status lbk_stream_mul_f64(lbk_ctx ctx, int64_t n, double scalar, const double* c, double* b)
+{
+    if (!ctx) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        check_n(n, "stream_mul");
+        need(pair_aligned(n, {b, c}), LBK_USAGE_ERROR, "stream_mul: even n and 16-B aligned arrays");
+        if (n == 0) return;
+        stream_mul_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+            n / 2, scalar, reinterpret_cast<const double2*>(c), reinterpret_cast<double2*>(b));
+        LBK_LAUNCH_CHECK();
+    });
+}
+
+lbk_status lbk_stream_add_f64(lbk_ctx ctx, int64_t n, const double* a, const double* b, double* c)
+{
+    if (!ctx) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        check_n(n, "stream_add");
+        need(pair_aligned(n, {a, b, c}), LBK_USAGE_ERROR,
+             "stream_add: even n and 16-B aligned arrays");
+        if (n == 0) return;
+        stream_add_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+            n / 2, reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b),
+            reinterpret_cast<double2*>(c));
+        LBK_LAUNCH_CHECK();
+    });
+}
+
+lbk_status lbk_stream_dot_f64(lbk_ctx ctx, int64_t n, const double* a, const double* b,
+                              double* result)
+{
+    return lbk_dot_f64(ctx, n, a, b, result);
+}
+
+lbk_status lbk_flops_sweep_f64(lbk_ctx ctx, int64_t n, int32_t fma_per_element, double* x)
+{
+    if (!ctx) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        check_n(n, "flops_sweep");
+        need(fma_per_element >= 0, LBK_USAGE_ERROR, "fma count must be nonnegative");
+        if (n == 0 || fma_per_element == 0) return;
+        flops_sweep_kernel<<<grid_for(ctx, n, 8), kThreads, 0, ctx->stream>>>(n, fma_per_element,
+                                                                               x);
         LBK_LAUNCH_CHECK();
     });
 }

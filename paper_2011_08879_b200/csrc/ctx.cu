@@ -35,9 +35,12 @@ void* scratch(lbk_ctx ctx, size_t bytes)
 
 RedWs red_ws(lbk_ctx ctx, int max_blocks, int slots)
 {
-    // Layout: [counter (256 B)] [out: 64 doubles] [partials]
-    const size_t need_bytes = 256 + 64 * sizeof(double) +
-                              size_t(max_blocks) * slots * sizeof(double);
+    // Layout: [counter (256 B)] [out: 64 doubles] [xacc: kXSlot int64]
+    //         [xout: kXOutSlots x kXSlot int64] [partials]
+    // counter, xacc and xout are zero between uses (every consumer re-zeroes).
+    const size_t xbytes = size_t(1 + kXOutSlots) * kXSlot * sizeof(long long);
+    const size_t head = 256 + 64 * sizeof(double) + xbytes;
+    const size_t need_bytes = head + size_t(max_blocks) * slots * sizeof(double);
     if (ctx->red.bytes < need_bytes) {
         if (ctx->red.ptr) {
             LBK_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -45,14 +48,16 @@ RedWs red_ws(lbk_ctx ctx, int max_blocks, int slots)
         }
         size_t want = need_bytes < (1u << 20) ? (1u << 20) : need_bytes;
         LBK_CUDA(cudaMalloc(&ctx->red.ptr, want));
-        LBK_CUDA(cudaMemsetAsync(ctx->red.ptr, 0, 256, ctx->stream));
+        LBK_CUDA(cudaMemsetAsync(ctx->red.ptr, 0, head, ctx->stream));
         ctx->red.bytes = want;
     }
     auto* base = static_cast<char*>(ctx->red.ptr);
     RedWs ws;
     ws.counter = reinterpret_cast<unsigned*>(base);
     ws.out = reinterpret_cast<double*>(base + 256);
-    ws.partials = reinterpret_cast<double*>(base + 256 + 64 * sizeof(double));
+    ws.xacc = reinterpret_cast<long long*>(base + 256 + 64 * sizeof(double));
+    ws.xout = ws.xacc + kXSlot;
+    ws.partials = reinterpret_cast<double*>(base + head);
     return ws;
 }
 

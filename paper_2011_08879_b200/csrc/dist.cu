@@ -95,6 +95,10 @@ struct NcclComm final : Comm {
     {
         LBK_NCCL(nccl().AllReduce(dev, dev, count, ncclDouble, ncclSum, comm, s));
     }
+    void allreduce_i64(long long* dev, int count, cudaStream_t s) override
+    {
+        LBK_NCCL(nccl().AllReduce(dev, dev, count, ncclInt64, ncclSum, comm, s));
+    }
     void exchange(const double* send_buf, const std::vector<int>& so, double* recv,
                   const std::vector<int>& ro, cudaStream_t s) override
     {
@@ -153,12 +157,15 @@ struct ThreadShared {
     int P;
     std::barrier<> bar;
     std::vector<double> slots[2];
+    std::vector<long long> islots[2];
     std::vector<const double*> send_bufs;
     std::vector<const std::vector<int>*> send_offs;
     explicit ThreadShared(int p) : P(p), bar(p), send_bufs(p), send_offs(p)
     {
         slots[0].resize(size_t(p) * 32);
         slots[1].resize(size_t(p) * 32);
+        islots[0].resize(size_t(p) * kXSlot);
+        islots[1].resize(size_t(p) * kXSlot);
     }
 };
 
@@ -179,6 +186,22 @@ struct ThreadComm final : Comm {
         for (int q = 0; q < nranks; ++q)
             for (int i = 0; i < count; ++i) tot[i] += slot[size_t(q) * 32 + i];
         LBK_CUDA(cudaMemcpyAsync(dev, tot, count * sizeof(double), cudaMemcpyHostToDevice, s));
+        LBK_CUDA(cudaStreamSynchronize(s));
+    }
+    void allreduce_i64(long long* dev, int count, cudaStream_t s) override
+    {
+        need(count <= kXSlot, LBK_USAGE_ERROR, "thread allreduce: too many limbs");
+        auto& slot = sh->islots[parity];
+        parity ^= 1;
+        LBK_CUDA(cudaMemcpyAsync(slot.data() + size_t(rank) * kXSlot, dev,
+                                 count * sizeof(long long), cudaMemcpyDeviceToHost, s));
+        LBK_CUDA(cudaStreamSynchronize(s));
+        sh->bar.arrive_and_wait();
+        long long tot[kXSlot];
+        for (int i = 0; i < count; ++i) tot[i] = 0;
+        for (int q = 0; q < nranks; ++q)
+            for (int i = 0; i < count; ++i) tot[i] += slot[size_t(q) * kXSlot + i];
+        LBK_CUDA(cudaMemcpyAsync(dev, tot, count * sizeof(long long), cudaMemcpyHostToDevice, s));
         LBK_CUDA(cudaStreamSynchronize(s));
     }
     void exchange(const double* send_buf, const std::vector<int>& so, double* recv,
@@ -225,6 +248,10 @@ struct PeerComm final : Comm {
     }
     void set_ready() { ready = true; }
     void allreduce_sum(double* dev, int count, cudaStream_t s) override;
+    void allreduce_i64(long long*, int, cudaStream_t) override
+    {
+        fail(LBK_INTERNAL, "peer communicator: exact reductions run in the finish kernels");
+    }
     void exchange(const double*, const std::vector<int>&, double*, const std::vector<int>&,
                   cudaStream_t) override
     {

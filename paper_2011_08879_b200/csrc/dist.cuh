@@ -46,6 +46,9 @@ struct Comm {
     // sum `count` doubles at dev over all ranks, result on every rank (same
     // bits everywhere), stream-ordered on s
     virtual void allreduce_sum(double* dev, int count, cudaStream_t s) = 0;
+    // sum `count` int64 at dev over all ranks (exact reductions, xred.cuh:
+    // integer sums are order-free), stream-ordered on s
+    virtual void allreduce_i64(long long* dev, int count, cudaStream_t s) = 0;
     // halo exchange: send_buf[send_off[q] .. send_off[q+1]) goes to rank q;
     // from rank q we receive recv_off[q+1]-recv_off[q] values into
     // recv + recv_off[q].  Stream-ordered on s.
@@ -113,11 +116,11 @@ struct MappedEpi {
         const int m = __ldg(map + r);
         return {m, EpiPre<Epi>::load(e, m)};
     }
-    __device__ void row_pre(int, double s, const Pre& p, double* acc) const
+    __device__ void row_pre(int, double s, const Pre& p, RAcc* acc) const
     {
         EpiPre<Epi>::row(e, p.r, s, p.p, acc);
     }
-    __device__ void row(int r, double s, double* acc) const { e.row(__ldg(map + r), s, acc); }
+    __device__ void row(int r, double s, RAcc* acc) const { e.row(__ldg(map + r), s, acc); }
     __device__ void finish(const double* t) const { e.finish(t); }
 };
 
@@ -128,7 +131,7 @@ struct OffsetEpiBase {
     int off;
     __device__ bool skip() const { return e.skip(); }
     __device__ void prefetch(int rb, int re) const { EpiPf<Epi>::run(e, rb + off, re + off); }
-    __device__ void row(int r, double s, double* acc) const { e.row(r + off, s, acc); }
+    __device__ void row(int r, double s, RAcc* acc) const { e.row(r + off, s, acc); }
     __device__ void finish(const double* t) const { e.finish(t); }
 };
 template <class Epi, class = void>
@@ -138,7 +141,7 @@ template <class Epi>
 struct OffsetEpi<Epi, std::void_t<typename Epi::Pre>> : OffsetEpiBase<Epi> {
     using Pre = typename Epi::Pre;
     __device__ Pre pre(int r) const { return this->e.pre(r + this->off); }
-    __device__ void row_pre(int r, double s, const Pre& p, double* acc) const
+    __device__ void row_pre(int r, double s, const Pre& p, RAcc* acc) const
     {
         this->e.row_pre(r + this->off, s, p, acc);
     }
@@ -202,10 +205,11 @@ __global__ void __launch_bounds__(256)
     const int par = static_cast<int>(e & 1);
     if (threadIdx.x <= pd.P) ro[threadIdx.x] = __ldg(recv_off + threadIdx.x);
     __syncthreads();
+    if constexpr (Epi::NV > 0) red_begin<NV>();
     const bool skip = epi.skip();
-    double acc[NV];
+    RAcc acc[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    for (int i = 0; i < NV; ++i) racc_zero(acc[i]);
     if (!skip) {
         for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows;
              i += gridDim.x * blockDim.x) {
@@ -232,14 +236,18 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     if (threadIdx.x == 0 && atomicAdd(&me->recv_cnt, 1u) == gridDim.x - 1) {
         me->recv_cnt = 0;
+        // hand back epoch e to EVERY peer, not only those we received
+        // from: the epoch counter is per communicator, so a peer that sent
+        // us nothing this epoch (another matrix sharing the communicator,
+        // with a different neighbour set) must still see it consumed
+        // (A,B,B,A over one communicator deadlocked)
         for (int q = 0; q < pd.P; ++q)
-            if (ro[q + 1] > ro[q]) st_volatile_u64(&pd.win[q]->empty[pd.rank], e);
+            if (q != pd.rank) st_volatile_u64(&pd.win[q]->empty[pd.rank], e);
         *reinterpret_cast<volatile unsigned long long*>(&me->seq_x) = e;
     }
     if constexpr (Epi::NV > 0) {
         if (skip) return;
-        block_sum<NV>(acc, threadIdx.x, blockDim.x, red_sh);
-        grid_reduce_finish<NV>(acc, ws, threadIdx.x, blockDim.x, red_sh,
+        grid_reduce<NV>(acc, ws, threadIdx.x, blockDim.x, red_sh,
                                [&](const double* tot) { epi.finish(tot); });
     }
 }

@@ -16,6 +16,7 @@
 #include <utility>
 
 #include "lbk.h"
+#include "xred.cuh"
 
 namespace lbk {
 
@@ -85,7 +86,13 @@ struct RedWs {
     int defer = 0;        // 1: the finisher only stores the grid totals to
                           // `out` (a cross-rank allreduce runs before the
                           // epilogue's finish(), see dist.cu)
+    long long* xacc = nullptr;  // exact mode: the grid's limb accumulator
+                                // (kXSlot int64, zero between uses)
+    long long* xout = nullptr;  // exact mode, defer: the slot the blocks add
+                                // their limbs into (consumer rounds + zeroes)
 };
+// exact-mode deferred slots in the reduction workspace (DistEnv)
+constexpr int kXOutSlots = 8;
 RedWs red_ws(lbk_ctx ctx, int max_blocks, int slots);
 
 constexpr int kRedMaxBlocks = 4096;
@@ -208,6 +215,37 @@ __device__ __forceinline__ T warp_sum(T v)
     return v;
 }
 
+// ------------------------------------------------ reduction accumulators
+// Every dot/norm of the path accumulates through racc_add.  Default: the
+// exact, partition-independent reduction (xred.cuh).  -DLBK_RED_TREE builds
+// the previous deterministic tree (per-lane double sums, block tree, block-
+// ordered grid sum) for A/B measurements; its results depend on the grid.
+#ifdef LBK_RED_TREE
+constexpr bool kExactRed = false;
+using RAcc = double;
+__device__ __forceinline__ void racc_zero(RAcc& a) { a = 0.0; }
+__device__ __forceinline__ void racc_add(RAcc* acc, int k, double t)
+{
+    acc[k] = __dadd_rn(acc[k], t);
+}
+#else
+constexpr bool kExactRed = true;
+using RAcc = XLane;
+__device__ __forceinline__ void racc_zero(RAcc& a) { xl_zero(a); }
+__device__ __forceinline__ void racc_add(RAcc* acc, int k, double t)
+{
+    xl_add(acc[k], t, g_xsh + k * kXV);
+}
+#endif
+
+// Kernel prologue of every reducing kernel (all threads, after any
+// block-uniform early exit): zeroes the block accumulator.
+template <int NV>
+__device__ __forceinline__ void red_begin()
+{
+    if constexpr (kExactRed) xred_begin<NV>();
+}
+
 // Block-wide sum of NV doubles over the first `nthreads` threads (all of
 // which must call).  Result valid in thread 0.  Fixed order => deterministic.
 template <int NV>
@@ -271,6 +309,51 @@ __device__ __forceinline__ bool grid_reduce_finish(const double (&v)[NV], RedWs 
         *ws.counter = 0;
     }
     return true;
+}
+
+// Kernel epilogue of every reducing kernel (all threads of the block):
+// reduces the lanes' accumulators over the grid; the last block calls
+// fin(totals) in thread 0 -- or, with ws.defer, leaves the grid totals for
+// the distributed consumer (tree: ws.out doubles; exact: ws.xout limbs).
+template <int NV, class Fin>
+__device__ __forceinline__ bool grid_reduce(RAcc (&acc)[NV], RedWs ws, int tid, int nthreads,
+                                            double* sh, Fin&& fin)
+{
+    if constexpr (!kExactRed) {
+        block_sum<NV>(acc, tid, nthreads, sh);
+        return grid_reduce_finish<NV>(acc, ws, tid, nthreads, sh, fin);
+    } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) xl_warp_flush(acc[v], g_xsh + v * kXV);
+        __syncthreads();
+        long long* G = ws.defer ? ws.xout : ws.xacc;
+        for (int i = tid; i < NV * kXV; i += nthreads) {
+            const long long v = g_xsh[i];
+            if (v) atomicAdd(reinterpret_cast<unsigned long long*>(G + i),
+                             static_cast<unsigned long long>(v));
+        }
+        if (ws.defer) return false;
+        __shared__ unsigned s_xlast;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_xlast = (atomicAdd(ws.counter, 1u) == gridDim.x - 1);
+        __syncthreads();
+        if (!s_xlast) return false;
+        __threadfence();
+        for (int i = tid; i < NV * kXV; i += nthreads) {
+            g_xsh[i] = __ldcg(G + i);
+            G[i] = 0;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double tot[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) tot[v] = xred_round(g_xsh + v * kXV);
+            fin(tot);
+            *ws.counter = 0;
+        }
+        return true;
+    }
 }
 
 // First statement of every kernel that may be launched with programmatic

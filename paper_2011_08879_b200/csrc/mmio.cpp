@@ -97,7 +97,10 @@ struct LineReader {
         const char* q = static_cast<const char*>(std::memchr(p, '\n', static_cast<size_t>(e - p)));
         const char* end = q ? q : e;
         out = std::string_view(p, static_cast<size_t>(end - p));
-        if (!out.empty() && out.back() == '\r') out.remove_suffix(1);  // getline keeps '\r'; be lenient
+        // '\r' is kept, as std::getline keeps it (io.cpp:77-137): it is
+        // whitespace to the tokenizer, so CRLF entry lines parse, and a CRLF
+        // blank line is non-empty -- rejected exactly where the reference
+        // rejects it (CRLF parity decided, tests/test_mmio.py)
         p = q ? q + 1 : e;
         ++no;
         return true;
@@ -136,7 +139,12 @@ void parse(const std::string& text, lbk_mm_s& m)
         if (nrows < 0 || ncols < 0 || nnz < 0) fail("negative size", rd.no);
         break;
     }
-    const size_t cap = static_cast<size_t>(symmetric ? 2 * nnz : nnz);
+    // nnz comes from the file: cap the reservation by what the text can
+    // hold (an entry line has >= 4 bytes), so a hostile header can neither
+    // overflow 2*nnz nor make reserve() throw
+    const int64_t fit = static_cast<int64_t>(text.size() / 4) + 1;
+    const int64_t want = nnz < fit ? nnz : fit;
+    const size_t cap = static_cast<size_t>(symmetric ? 2 * want : want);
     m.rows.reserve(cap);
     m.cols.reserve(cap);
     m.vals.reserve(cap);
@@ -208,6 +216,12 @@ lbk_status lbk_mm_read(const char* path, lbk_mm* out)
     } catch (const std::bad_alloc&) {
         g_mm_err = "host allocation failed";
         return LBK_OUT_OF_MEMORY;
+    } catch (const std::length_error&) {
+        g_mm_err = "host allocation failed (size)";
+        return LBK_OUT_OF_MEMORY;
+    } catch (const std::exception& e) {  // nothing may cross the C ABI
+        g_mm_err = e.what();
+        return LBK_FORMAT_ERROR;
     }
 }
 

@@ -44,6 +44,9 @@ struct PeerHdr {
     // {epoch:32 | half:32}, [parity][source rank][value][half]; a word is
     // valid when its epoch tag matches, so no fences or flags are needed
     unsigned long long red_ll[2][kPeerMax][kPeerRedMax][2];
+    // exact-reduction mailbox (xred.cuh): per value a header word then its
+    // sign-magnitude 32-bit digits, LL-tagged; [parity][source][word]
+    unsigned long long xred_ll[2][kPeerMax][kXSlot];
     unsigned long long seq_x, seq_r;     // local epochs (this rank only)
     unsigned int recv_cnt, pad0_;        // last-block counter
     int error;
@@ -142,6 +145,33 @@ __device__ __forceinline__ double peer_ll_read(const unsigned long long* w, unsi
     return __longlong_as_double(static_cast<long long>((b << 32) | (a & 0xffffffffull)));
 }
 
+// One LL word: spin until its tag is e32; returns the 32-bit payload.
+__device__ __forceinline__ unsigned peer_ll_read32(const unsigned long long* w, unsigned e32,
+                                                   PeerHdr* me, int what, int peer,
+                                                   unsigned long long e)
+{
+    unsigned long long a = ld_volatile_u64(w);
+    if (static_cast<unsigned>(a >> 32) != e32) {
+        const unsigned long long t0 = global_ns();
+        for (;;) {
+            a = ld_volatile_u64(w);
+            if (static_cast<unsigned>(a >> 32) == e32) break;
+            if (*reinterpret_cast<volatile int*>(&me->error)) break;
+            if (global_ns() - t0 > static_cast<unsigned long long>(me->timeout_ns)) {
+                if (atomicExch(&me->error, 1) == 0) {
+                    me->err_info[0] = what;
+                    me->err_info[1] = peer;
+                    me->err_info[2] = static_cast<long long>(e);
+                    me->err_info[3] = static_cast<long long>(a >> 32);
+                }
+                break;
+            }
+            __nanosleep(32);
+        }
+    }
+    return static_cast<unsigned>(a);
+}
+
 __device__ __forceinline__ void peer_ll_store(unsigned long long* w, double v,
                                               unsigned long long tag)
 {
@@ -185,6 +215,86 @@ __device__ __forceinline__ double peer_allreduce_warp(const PeerDev& pd, double 
     __syncwarp();
     if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(&me->seq_r) = e;
     return t;
+}
+
+// Exact variant (xred.cuh).  One warp.  L (shared memory) holds nv values
+// of raw limbs (kXV int64 each) -- this rank's exact totals; on return it
+// holds the exact sum over all ranks (raw limbs, round with xred_round).
+// Each rank posts every value as a header {lo:8 | cnt:8 | neg:1 | pinf:1 |
+// ninf:1 | nan:1} and cnt sign-magnitude digits; integer sums make the
+// result independent of rank order and of the partition.
+__device__ __forceinline__ void peer_xallreduce_warp(const PeerDev& pd, long long* L, int nv)
+{
+    const int lane = threadIdx.x & 31;
+    PeerHdr* me = pd.win[pd.rank];
+    __shared__ unsigned hdr[kXMaxNV];
+    if (lane == 0) {
+        for (int v = 0; v < nv; ++v) {
+            long long* X = L + v * kXV;
+            long long c = 0;
+            for (int i = 0; i < kXL; ++i) {
+                const long long t = X[i] + c;
+                c = t >> 32;
+                X[i] = t & 0xffffffffLL;
+            }
+            const bool neg = c < 0;
+            if (neg) {
+                long long cy = 1;
+                for (int i = 0; i < kXL; ++i) {
+                    const long long t = (0xffffffffLL - X[i]) + cy;
+                    cy = t >> 32;
+                    X[i] = t & 0xffffffffLL;
+                }
+            }
+            int lo = 0, hi = -1;
+            for (int i = 0; i < kXL; ++i)
+                if (X[i]) {
+                    if (hi < 0) lo = i;
+                    hi = i;
+                }
+            const int cnt = hi < 0 ? 0 : hi - lo + 1;
+            hdr[v] = static_cast<unsigned>(lo) | (static_cast<unsigned>(cnt) << 8) |
+                     (neg ? 1u << 16 : 0u) | (X[kXPinf] ? 1u << 17 : 0u) |
+                     (X[kXNinf] ? 1u << 18 : 0u) | (X[kXNan] ? 1u << 19 : 0u);
+        }
+    }
+    __syncwarp();
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&me->seq_r) + 1;
+    const int par = static_cast<int>(e & 1);
+    const unsigned e32 = static_cast<unsigned>(e);
+    const unsigned long long tag = static_cast<unsigned long long>(e32) << 32;
+    for (int v = 0; v < nv; ++v) {
+        const unsigned h = hdr[v];
+        const int lo = h & 0xff, cnt = (h >> 8) & 0xff;
+        for (int w = lane; w <= cnt; w += 32) {
+            const unsigned pay = w == 0 ? h : static_cast<unsigned>(L[v * kXV + lo + w - 1]);
+            for (int q = 0; q < pd.P; ++q)
+                st_volatile_u64(&pd.win[q]->xred_ll[par][pd.rank][v * kXV + w], tag | pay);
+        }
+    }
+    __syncwarp();
+    for (int i = lane; i < nv * kXV; i += 32) L[i] = 0;
+    __syncwarp();
+    for (int q = 0; q < pd.P; ++q) {
+        for (int v = 0; v < nv; ++v) {
+            const unsigned long long* box = me->xred_ll[par][q] + v * kXV;
+            const unsigned h = peer_ll_read32(box, e32, me, 2, q, e);
+            const int lo = h & 0xff, cnt = (h >> 8) & 0xff;
+            const bool neg = (h >> 16) & 1;
+            for (int w = lane; w < cnt; w += 32) {
+                const long long d = peer_ll_read32(box + 1 + w, e32, me, 2, q, e);
+                L[v * kXV + lo + w] += neg ? -d : d;
+            }
+            if (lane == 0) {
+                L[v * kXV + kXPinf] += (h >> 17) & 1;
+                L[v * kXV + kXNinf] += (h >> 18) & 1;
+                L[v * kXV + kXNan] += (h >> 19) & 1;
+            }
+            __syncwarp();
+        }
+    }
+    if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(&me->seq_r) = e;
+    __syncwarp();
 }
 
 }  // namespace lbk

@@ -126,15 +126,15 @@ struct EpiInit {
         l2_prefetch_rows(b, rb, re);
     }
     __device__ Pre pre(int i) const { return {b[i]}; }
-    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
+    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
     {
         const double v = add_rn(pr.b, -s);
         r[i] = v;
         p[i] = v;
         if (rt) rt[i] = v;
         if (u) u[i] = v;
-        acc[0] = add_rn(acc[0], mul_rn(v, v));
+        racc_add(acc, 0, mul_rn(v, v));
     }
     __device__ void finish(const double* tot) const
     {
@@ -175,11 +175,11 @@ struct EpiCgK1 {
         double p;
     };
     __device__ Pre pre(int i) const { return {p[i]}; }
-    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
+    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
     {
         q[i] = s;
-        acc[0] = add_rn(acc[0], mul_rn(pr.p, s));
+        racc_add(acc, 0, mul_rn(pr.p, s));
     }
     __device__ void finish(const double* tot) const
     {
@@ -213,11 +213,11 @@ struct EpiCgK3 {
         double b, p, r;
     };
     __device__ Pre pre(int i) const { return {b[i], p[i], r[i]}; }
-    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
+    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
     {
         const double t = add_rn(pr.b, -s);
-        acc[0] = add_rn(acc[0], mul_rn(t, t));
+        racc_add(acc, 0, mul_rn(t, t));
         const double beta = st->beta;
         p[i] = add_rn(mul_rn(pr.p, beta), pr.r);
     }
@@ -271,11 +271,11 @@ struct EpiTrueRes {
         l2_prefetch_rows(b, rb, re);
     }
     __device__ Pre pre(int i) const { return {b[i]}; }
-    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int, double s, const Pre& pr, double* acc) const
+    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int, double s, const Pre& pr, RAcc* acc) const
     {
         const double t = add_rn(pr.b, -s);
-        acc[0] = add_rn(acc[0], mul_rn(t, t));
+        racc_add(acc, 0, mul_rn(t, t));
     }
     __device__ void finish(const double* tot) const
     {
@@ -319,11 +319,11 @@ struct EpiBiB2 {
         l2_prefetch_rows(rt, rb, re);
     }
     __device__ Pre pre(int i) const { return {rt[i]}; }
-    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
+    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
     {
         v[i] = s;
-        acc[0] = add_rn(acc[0], mul_rn(pr.rt, s));
+        racc_add(acc, 0, mul_rn(pr.rt, s));
     }
     __device__ void finish(const double* tot) const
     {
@@ -352,12 +352,12 @@ struct EpiBiB4 {
         l2_prefetch_rows(s, rb, re);
     }
     __device__ Pre pre(int i) const { return {s[i]}; }
-    __device__ void row(int i, double sum, double* acc) const { row_pre(i, sum, pre(i), acc); }
-    __device__ void row_pre(int i, double sum, const Pre& pr, double* acc) const
+    __device__ void row(int i, double sum, RAcc* acc) const { row_pre(i, sum, pre(i), acc); }
+    __device__ void row_pre(int i, double sum, const Pre& pr, RAcc* acc) const
     {
         t[i] = sum;
-        acc[0] = add_rn(acc[0], mul_rn(sum, sum));
-        acc[1] = add_rn(acc[1], mul_rn(sum, pr.s));
+        racc_add(acc, 0, mul_rn(sum, sum));
+        racc_add(acc, 1, mul_rn(sum, pr.s));
     }
     __device__ void finish(const double* tot) const
     {
@@ -396,11 +396,11 @@ struct EpiBiB6 {
         l2_prefetch_rows(r, rb, re);
     }
     __device__ Pre pre(int i) const { return {b[i], p[i], v[i], r[i]}; }
-    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
+    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
     {
         const double t = add_rn(pr.b, -s);
-        acc[0] = add_rn(acc[0], mul_rn(t, t));
+        racc_add(acc, 0, mul_rn(t, t));
         const double beta = st->beta, omega = st->omega;
         p[i] = add_rn(mul_rn(add_rn(pr.p, mul_rn(-omega, pr.v)), beta), pr.r);
     }
@@ -461,11 +461,11 @@ struct EpiCgsV {
         l2_prefetch_rows(rt, rb, re);
     }
     __device__ Pre pre(int i) const { return {rt[i]}; }
-    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
+    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
     {
         v[i] = s;
-        acc[0] = add_rn(acc[0], mul_rn(pr.rt, s));
+        racc_add(acc, 0, mul_rn(pr.rt, s));
     }
     __device__ void finish(const double* tot) const
     {
@@ -499,15 +499,15 @@ struct EpiCgsT {
         l2_prefetch_rows(rt, rb, re);
     }
     __device__ Pre pre(int i) const { return {x[i], r[i], w[i], rt[i]}; }
-    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
+    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
     {
         const double a = st->alpha;
         t[i] = s;
         x[i] = add_rn(pr.x, mul_rn(a, pr.w));
         const double rn = add_rn(pr.r, mul_rn(-a, s));
         r[i] = rn;
-        acc[0] = add_rn(acc[0], mul_rn(pr.rt, rn));
+        racc_add(acc, 0, mul_rn(pr.rt, rn));
     }
     __device__ void finish(const double* tot) const
     {
@@ -530,11 +530,11 @@ struct EpiCgsRes {
         l2_prefetch_rows(b, rb, re);
     }
     __device__ Pre pre(int i) const { return {b[i]}; }
-    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int, double s, const Pre& pr, double* acc) const
+    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int, double s, const Pre& pr, RAcc* acc) const
     {
         const double t = add_rn(pr.b, -s);
-        acc[0] = add_rn(acc[0], mul_rn(t, t));
+        racc_add(acc, 0, mul_rn(t, t));
     }
     __device__ void finish(const double* tot) const
     {
@@ -599,12 +599,12 @@ struct EpiGmRes {
         l2_prefetch_rows(b, rb, re);
     }
     __device__ Pre pre(int i) const { return {b[i]}; }
-    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
+    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
     {
         const double t = add_rn(pr.b, -s);
         v0[i] = t;
-        acc[0] = add_rn(acc[0], mul_rn(t, t));
+        racc_add(acc, 0, mul_rn(t, t));
     }
     __device__ void finish(const double* tot) const
     {
@@ -678,11 +678,11 @@ struct EpiGmApply {
         l2_prefetch_rows(v0, rb, re);
     }
     __device__ Pre pre(int i) const { return {v0[i]}; }
-    __device__ void row(int i, double s, double* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, double* acc) const
+    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
     {
         w[i] = s;
-        acc[0] = add_rn(acc[0], mul_rn(pr.v0, s));
+        racc_add(acc, 0, mul_rn(pr.v0, s));
     }
     __device__ void finish(const double* tot) const
     {
@@ -709,16 +709,16 @@ __global__ void __launch_bounds__(256) vec_kernel(long long n, Op op, RedWs ws)
     constexpr int NV = Op::NV;
     __shared__ double sh[32 * NV];
     if (op.skip()) return;
-    double acc[NV];
+    if constexpr (!NoFinish<Op>::value) red_begin<NV>();
+    RAcc acc[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    for (int i = 0; i < NV; ++i) racc_zero(acc[i]);
     op.prologue();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         op.elem(i, acc);
     if constexpr (!NoFinish<Op>::value) {
-        block_sum<NV>(acc, threadIdx.x, blockDim.x, sh);
-        grid_reduce_finish<NV>(acc, ws, threadIdx.x, blockDim.x, sh,
+        grid_reduce<NV>(acc, ws, threadIdx.x, blockDim.x, sh,
                                [&](const double* tot) { op.finish(tot); });
     }
 }
@@ -735,12 +735,12 @@ struct OpCgK2 {
     double alpha;
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     __device__ void prologue() { alpha = st->alpha; }
-    __device__ void elem(long long i, double* acc) const
+    __device__ void elem(long long i, RAcc* acc) const
     {
         x[i] = add_rn(x[i], mul_rn(alpha, p[i]));
         const double rn = add_rn(r[i], mul_rn(-alpha, q[i]));
         r[i] = rn;
-        acc[0] = add_rn(acc[0], mul_rn(rn, rn));
+        racc_add(acc, 0, mul_rn(rn, rn));
     }
     __device__ void finish(const double* tot) const
     {
@@ -778,7 +778,7 @@ struct OpCgP {
     double beta;
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     __device__ void prologue() { beta = st->beta; }
-    __device__ void elem(long long i, double*) const { p[i] = add_rn(mul_rn(p[i], beta), r[i]); }
+    __device__ void elem(long long i, RAcc*) const { p[i] = add_rn(mul_rn(p[i], beta), r[i]); }
     static constexpr bool kNoFinish = true;  // nothing to reduce
     __device__ void finish(const double*) const {}
 };
@@ -793,11 +793,11 @@ struct OpBiB3 {
     double alpha;
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     __device__ void prologue() { alpha = st->alpha; }
-    __device__ void elem(long long i, double* acc) const
+    __device__ void elem(long long i, RAcc* acc) const
     {
         const double sv = add_rn(r[i], mul_rn(-alpha, v[i]));
         s[i] = sv;
-        acc[0] = add_rn(acc[0], mul_rn(sv, sv));
+        racc_add(acc, 0, mul_rn(sv, sv));
     }
     __device__ void finish(const double* tot) const
     {
@@ -823,13 +823,13 @@ struct OpBiB5 {
         alpha = st->alpha;
         omega = st->omega;
     }
-    __device__ void elem(long long i, double* acc) const
+    __device__ void elem(long long i, RAcc* acc) const
     {
         const double si = s[i];
         x[i] = add_rn(add_rn(x[i], mul_rn(alpha, p[i])), mul_rn(omega, si));
         const double rn = add_rn(si, mul_rn(-omega, t[i]));
         r[i] = rn;
-        acc[0] = add_rn(acc[0], mul_rn(rt[i], rn));
+        racc_add(acc, 0, mul_rn(rt[i], rn));
     }
     __device__ void finish(const double* tot) const
     {
@@ -856,7 +856,7 @@ struct OpCgsUP {
         return *(volatile int*)&st->done != 0 || *(volatile int*)&st->iter <= 1;
     }
     __device__ void prologue() { beta = st->beta; }
-    __device__ void elem(long long i, double*) const
+    __device__ void elem(long long i, RAcc*) const
     {
         const double qi = q[i];
         const double ui = add_rn(mul_rn(qi, beta), r[i]);
@@ -879,7 +879,7 @@ struct OpCgsQW {
     double alpha;
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     __device__ void prologue() { alpha = st->alpha; }
-    __device__ void elem(long long i, double*) const
+    __device__ void elem(long long i, RAcc*) const
     {
         const double ui = u[i];
         const double qi = add_rn(ui, mul_rn(-alpha, v[i]));
@@ -903,11 +903,11 @@ struct OpGmMgs {
     double h;
     __device__ bool skip() const { return gm_step_skip(st, jj); }
     __device__ void prologue() { h = st->gm->H[(i - 1) * st->gm->restart + jj]; }
-    __device__ void elem(long long k, double* acc) const
+    __device__ void elem(long long k, RAcc* acc) const
     {
         const double wn = add_rn(w[k], mul_rn(-h, vprev[k]));
         w[k] = wn;
-        acc[0] = add_rn(acc[0], mul_rn(vi ? vi[k] : wn, wn));
+        racc_add(acc, 0, mul_rn(vi ? vi[k] : wn, wn));
     }
     __device__ void finish(const double* tot) const
     {
@@ -960,7 +960,7 @@ struct OpGmScale {
     double inv;
     __device__ bool skip() const { return gm_step_skip(st, jj); }
     __device__ void prologue() { inv = 1.0 / (w ? st->gm->hnext : st->gm->beta); }
-    __device__ void elem(long long k, double*) const { v[k] = mul_rn(w ? w[k] : v[k], inv); }
+    __device__ void elem(long long k, RAcc*) const { v[k] = mul_rn(w ? w[k] : v[k], inv); }
     static constexpr bool kNoFinish = true;  // nothing to reduce
     __device__ void finish(const double*) const {}
 };
@@ -993,7 +993,7 @@ struct OpGmUpdate {
     int steps;
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     __device__ void prologue() { steps = st->gm->steps; }
-    __device__ void elem(long long k, double*) const
+    __device__ void elem(long long k, RAcc*) const
     {
         const double* y = st->gm->y;
         double v = x[k];
@@ -1206,6 +1206,126 @@ __global__ void peer_flush_cg_kernel(E3 e3, const double* base, int has_a, int h
     }
 }
 
+// Exact mode (xred.cuh): the fused kernels of a rank add their limbs into
+// one deferred slot (interior and boundary rows alike -- integer sums need
+// no combine step); the slot is summed over ranks (NCCL int64 allreduce /
+// host sums / peer digit posts) and rounded once, so every rank and every
+// rank count sees the same bits as the single-GPU solver.
+template <class E>
+__global__ void xfinish_kernel(E e, long long* slot)
+{
+    constexpr int NV = E::NV > 0 ? E::NV : 1;
+    __shared__ long long L[NV * kXV];
+    if (e.skip()) return;
+    for (int i = threadIdx.x; i < NV * kXV; i += blockDim.x) {
+        L[i] = slot[i];
+        slot[i] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) t[v] = xred_round(L + v * kXV);
+        e.finish(t);
+    }
+}
+
+template <class E>
+__global__ void peer_xfinish_kernel(E e, long long* slot, PeerDev pd)
+{
+    pdl_enter();
+    constexpr int NV = E::NV > 0 ? E::NV : 1;
+    __shared__ long long L[NV * kXV];
+    if (e.skip()) return;
+    const int lane = threadIdx.x;
+    for (int i = lane; i < NV * kXV; i += 32) {
+        L[i] = slot[i];
+        slot[i] = 0;
+    }
+    __syncwarp();
+    peer_xallreduce_warp(pd, L, NV);
+    if (lane == 0) {
+        double t[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) t[v] = xred_round(L + v * kXV);
+        e.finish(t);
+    }
+}
+
+// exact-mode twin of peer_finish_cg_kernel: K1's <p,Ap> (slot s1) and the
+// pending K3 residual (slot s3) travel in one exchange
+template <class E1, class E3>
+__global__ void peer_xfinish_cg_kernel(E1 e1, E3 e3, long long* s1, long long* s3, PeerDev pd)
+{
+    pdl_enter();
+    __shared__ long long L[2 * kXV];
+    if (e1.skip()) return;
+    const int lane = threadIdx.x;
+    const bool pending = e1.st->res_pending != 0;
+    for (int i = lane; i < kXV; i += 32) {
+        L[i] = s1[i];
+        s1[i] = 0;
+        L[kXV + i] = pending ? s3[i] : 0;
+        if (pending) s3[i] = 0;
+    }
+    __syncwarp();
+    // the pending residual goes first so its finish runs before K1's
+    if (pending) {
+        for (int i = lane; i < kXV; i += 32) {
+            const long long a = L[i];
+            L[i] = L[kXV + i];
+            L[kXV + i] = a;
+        }
+        __syncwarp();
+    }
+    peer_xallreduce_warp(pd, L, pending ? 2 : 1);
+    if (lane == 0) {
+        if (pending) {
+            const double t3 = xred_round(L);
+            e3.finish(&t3);
+            if (e1.st->done) return;
+        }
+        const double t1 = xred_round(pending ? L + kXV : L);
+        e1.finish(&t1);
+        e1.st->res_pending = 1;
+    }
+}
+
+template <class E3>
+__global__ void peer_xflush_cg_kernel(E3 e3, long long* s3, PeerDev pd)
+{
+    pdl_enter();
+    __shared__ long long L[kXV];
+    if (e3.skip() || !e3.st->res_pending) return;
+    const int lane = threadIdx.x;
+    for (int i = lane; i < kXV; i += 32) {
+        L[i] = s3[i];
+        s3[i] = 0;
+    }
+    __syncwarp();
+    peer_xallreduce_warp(pd, L, 1);
+    if (lane == 0) {
+        const double t = xred_round(L);
+        e3.finish(&t);
+    }
+}
+
+// ||b|| of the distributed right-hand side (exact mode)
+struct OpSelfDot {
+    static constexpr int NV = 1;
+    const double* __restrict__ b;
+    __device__ bool skip() const { return false; }
+    __device__ void prologue() {}
+    __device__ void elem(long long i, RAcc* acc) const { racc_add(acc, 0, mul_rn(b[i], b[i])); }
+    __device__ void finish(const double*) const {}
+};
+struct EpiSqrtTot {
+    static constexpr int NV = 1;
+    double* out;
+    __device__ bool skip() const { return false; }
+    __device__ void finish(const double* t) const { *out = sqrt(t[0]); }
+};
+
 struct DistEnv {
     static constexpr bool kMergeCg = true;
     lbk_ctx ctx;
@@ -1244,9 +1364,35 @@ struct DistEnv {
         finish_kernel<E><<<1, 1, 0, ctx->stream>>>(e, ws.out + 16);
         LBK_LAUNCH_CHECK();
     }
+    long long* xslot(int k) const { return ws.xout + size_t(k) * kXSlot; }
+    // exact mode: sum slot k over the ranks, round, finish()
+    template <class E>
+    void finish_x(const E& e, int k)
+    {
+        if (const PeerDev* pd = comm ? comm->peer() : nullptr) {
+            launch_pdl(ctx, peer_xfinish_kernel<E>, dim3(1), dim3(32), 0, e, xslot(k), *pd);
+            LBK_LAUNCH_CHECK();
+            return;
+        }
+        if (reduce()) comm->allreduce_i64(xslot(k), (E::NV > 0 ? E::NV : 1) * kXV, ctx->stream);
+        xfinish_kernel<E><<<1, 32, 0, ctx->stream>>>(e, xslot(k));
+        LBK_LAUNCH_CHECK();
+    }
+    RedWs deferred(int k) const
+    {
+        RedWs w = ws;
+        w.defer = 1;
+        w.xout = xslot(k);
+        return w;
+    }
     template <class Epi>
     void apply(double* x, const Epi& e)
     {
+        if constexpr (kExactRed) {
+            dist_apply(ctx, D, comm, x, e, deferred(0), deferred(0));
+            finish_x(e, 0);
+            return;
+        }
         RedWs wa = ws, wb = ws;
         wa.defer = wb.defer = 1;
         wb.out = ws.out + 8;
@@ -1262,6 +1408,13 @@ struct DistEnv {
     template <class E1, class E3>
     void apply_k1_merged(double* x, const E1& e1, const E3& e3)
     {
+        if constexpr (kExactRed) {
+            dist_apply(ctx, D, comm, x, e1, deferred(0), deferred(0));
+            launch_pdl(ctx, peer_xfinish_cg_kernel<E1, E3>, dim3(1), dim3(32), 0, e1, e3,
+                       xslot(0), xslot(1), *comm->peer());
+            LBK_LAUNCH_CHECK();
+            return;
+        }
         RedWs wa = ws, wb = ws;
         wa.defer = wb.defer = 1;
         wb.out = ws.out + 8;
@@ -1273,6 +1426,10 @@ struct DistEnv {
     template <class E3>
     void apply_k3_deferred(double* x, const E3& e3)
     {
+        if constexpr (kExactRed) {
+            dist_apply(ctx, D, comm, x, e3, deferred(1), deferred(1));
+            return;
+        }
         RedWs wa = ws, wb = ws;
         wa.defer = wb.defer = 1;
         wa.out = ws.out + 32;
@@ -1282,6 +1439,12 @@ struct DistEnv {
     template <class E3>
     void flush_k3(const E3& e3)
     {
+        if constexpr (kExactRed) {
+            launch_pdl(ctx, peer_xflush_cg_kernel<E3>, dim3(1), dim3(32), 0, e3, xslot(1),
+                       *comm->peer());
+            LBK_LAUNCH_CHECK();
+            return;
+        }
         launch_pdl(ctx, peer_flush_cg_kernel<E3>, dim3(1), dim3(32), 0, e3, ws.out,
                    D->interior.nrows > 0 ? 1 : 0, D->boundary.nrows > 0 ? 1 : 0, *comm->peer());
         LBK_LAUNCH_CHECK();
@@ -1289,6 +1452,11 @@ struct DistEnv {
     template <class Op>
     void vec(const Op& o)
     {
+        if constexpr (kExactRed) {
+            launch_vec(ctx, D->n_local, o, deferred(0));
+            if constexpr (!NoFinish<Op>::value) finish_x(o, 0);
+            return;
+        }
         RedWs wa = ws;
         wa.defer = 1;
         launch_vec(ctx, D->n_local, o, wa);
@@ -1301,6 +1469,15 @@ struct DistEnv {
     }
     double norm(const double* b)
     {
+        if constexpr (kExactRed) {
+            launch_vec(ctx, D->n_local, OpSelfDot{b}, deferred(2));
+            finish_x(EpiSqrtTot{ws.out + 24}, 2);
+            double v = 0.0;
+            LBK_CUDA(cudaMemcpyAsync(&v, ws.out + 24, sizeof(double), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+            sync();
+            return v;
+        }
         double* d = ws.out + 24;
         if (lbk_dot_f64_dev(ctx, D->n_local, b, b, d) != LBK_OK) fail(LBK_CUDA_ERROR, ctx->err);
         if (reduce()) comm->allreduce_sum(d, 1, ctx->stream);
@@ -1647,6 +1824,9 @@ lbk_status lbk_dist_solve(lbk_ctx ctx, lbk_dist_csr D, lbk_comm comm, const doub
         need(D->P == 1 || (comm && comm->impl->nranks == D->P && comm->impl->rank == D->rank),
              LBK_USAGE_ERROR, "dist solve: communicator does not match the partition");
         DistEnv env{ctx, D, comm ? comm->impl : nullptr, red_ws(ctx, kRedMaxBlocks, 2)};
+        if constexpr (kExactRed)  // the deferred slots start every solve at zero
+            LBK_CUDA(cudaMemsetAsync(env.ws.xout, 0, size_t(kXOutSlots) * kXSlot * sizeof(long long),
+                                     ctx->stream));
         solve_impl(ctx, env, b, x, cfg, result, history, history_cap);
     });
 }

@@ -71,7 +71,7 @@ struct EpiStore {
     static constexpr int NV = 0;
     T* __restrict__ y;
     __device__ bool skip() const { return false; }
-    __device__ void row(int r, T s, double*) const { y[r] = s; }
+    __device__ void row(int r, T s, RAcc*) const { y[r] = s; }
     __device__ void finish(const double*) const {}
 };
 
@@ -90,13 +90,13 @@ struct EpiAxpby {
             if (beta != T(0)) l2_prefetch_rows(reinterpret_cast<const double*>(y), rb, re);
     }
     __device__ Pre pre(int r) const { return {beta != T(0) ? y[r] : T(0)}; }
-    __device__ void row_pre(int r, T s, const Pre& p, double*) const
+    __device__ void row_pre(int r, T s, const Pre& p, RAcc*) const
     {
         T v = mul_rn(alpha, s);
         if (beta != T(0)) v = add_rn(v, mul_rn(beta, p.y));
         y[r] = v;
     }
-    __device__ void row(int r, T s, double* acc) const { row_pre(r, s, pre(r), acc); }
+    __device__ void row(int r, T s, RAcc* acc) const { row_pre(r, s, pre(r), acc); }
     __device__ void finish(const double*) const {}
 };
 
@@ -253,7 +253,7 @@ struct EpiPre {
     struct type {};
     __device__ static type load(const Epi&, int) { return {}; }
     template <typename T>
-    __device__ static void row(const Epi& e, int r, T s, const type&, double* acc)
+    __device__ static void row(const Epi& e, int r, T s, const type&, RAcc* acc)
     {
         e.row(r, s, acc);
     }
@@ -264,7 +264,7 @@ struct EpiPre<Epi, std::void_t<typename Epi::Pre>> {
     using type = typename Epi::Pre;
     __device__ static type load(const Epi& e, int r) { return e.pre(r); }
     template <typename T>
-    __device__ static void row(const Epi& e, int r, T s, const type& p, double* acc)
+    __device__ static void row(const Epi& e, int r, T s, const type& p, RAcc* acc)
     {
         e.row_pre(r, s, p, acc);
     }
@@ -305,7 +305,7 @@ constexpr int kSeqRow = 256;  // staged rows up to this length stay bit-exact
 template <typename T, int G, class Epi, class Starts>
 __device__ __forceinline__ void staged_rows(int rb, int re, T* sv, const int* sc,
                                             const T* __restrict__ x, const Epi& epi,
-                                            double* acc, Starts&& starts)
+                                            RAcc* acc, Starts&& starts)
 {
     using EP = EpiPre<Epi>;
     constexpr int CH = 32 / G;
@@ -571,10 +571,11 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
     __shared__ __align__(8) uint64_t bars[Cfg::kWarps][Cfg::kSlots];
     __shared__ double red_sh[32 * NV];
     if (epi.skip()) return;
+    if constexpr (Epi::NV > 0) red_begin<NV>();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double acc[NV];
+    RAcc acc[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    for (int i = 0; i < NV; ++i) racc_zero(acc[i]);
 
     struct RowPf {
         int v[G + 1];
@@ -627,8 +628,7 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
 
     if constexpr (Epi::NV > 0) {
         __syncthreads();
-        block_sum<NV>(acc, tid, Cfg::kThreads, red_sh);
-        grid_reduce_finish<NV>(acc, ws, tid, Cfg::kThreads, red_sh,
+        grid_reduce<NV>(acc, ws, tid, Cfg::kThreads, red_sh,
                                [&](const double* tot) { epi.finish(tot); });
     }
 }
@@ -654,10 +654,11 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
     __shared__ __align__(8) uint64_t bars[Cfg::kWarps][Cfg::kSlots];
     __shared__ double red_sh[32 * NV];
     if (epi.skip()) return;
+    if constexpr (Epi::NV > 0) red_begin<NV>();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double acc[NV];
+    RAcc acc[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    for (int i = 0; i < NV; ++i) racc_zero(acc[i]);
 
     // one slice (its slice set a, length len), its column block read
     // through colv(a, j, v, c)
@@ -735,8 +736,7 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
 
     if constexpr (Epi::NV > 0) {
         __syncthreads();
-        block_sum<NV>(acc, tid, Cfg::kThreads, red_sh);
-        grid_reduce_finish<NV>(acc, ws, tid, Cfg::kThreads, red_sh,
+        grid_reduce<NV>(acc, ws, tid, Cfg::kThreads, red_sh,
                                [&](const double* tot) { epi.finish(tot); });
     }
 }
@@ -759,10 +759,11 @@ __global__ void __launch_bounds__((StreamCfg<T, 2>::kThreads), 2)
     __shared__ __align__(8) uint64_t bars[Cfg::kWarps][Cfg::kSlots];
     __shared__ double red_sh[32 * NV];
     if (epi.skip()) return;
+    if constexpr (Epi::NV > 0) red_begin<NV>();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double acc[NV];
+    RAcc acc[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    for (int i = 0; i < NV; ++i) racc_zero(acc[i]);
 
     struct NoPf {};
     warp_tile_loop<T, 2>(
@@ -818,8 +819,7 @@ __global__ void __launch_bounds__((StreamCfg<T, 2>::kThreads), 2)
 
     if constexpr (Epi::NV > 0) {
         __syncthreads();
-        block_sum<NV>(acc, tid, Cfg::kThreads, red_sh);
-        grid_reduce_finish<NV>(acc, ws, tid, Cfg::kThreads, red_sh,
+        grid_reduce<NV>(acc, ws, tid, Cfg::kThreads, red_sh,
                                [&](const double* tot) { epi.finish(tot); });
     }
 }
@@ -890,9 +890,10 @@ __global__ void __launch_bounds__(256)
     constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
     __shared__ double red_sh[32 * NV];
     if (epi.skip()) return;
-    double acc[NV];
+    if constexpr (Epi::NV > 0) red_begin<NV>();
+    RAcc acc[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    for (int i = 0; i < NV; ++i) racc_zero(acc[i]);
     const long long nquads = (static_cast<long long>(nrows) + 3) / 4;
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nquads;
          q += (long long)gridDim.x * blockDim.x) {
@@ -973,8 +974,7 @@ __global__ void __launch_bounds__(256)
             if (r0 + i < nrows) epi.row(r0 + i, sum[i], acc);
     }
     if constexpr (Epi::NV > 0) {
-        block_sum<NV>(acc, threadIdx.x, blockDim.x, red_sh);
-        grid_reduce_finish<NV>(acc, ws, threadIdx.x, blockDim.x, red_sh,
+        grid_reduce<NV>(acc, ws, threadIdx.x, blockDim.x, red_sh,
                                [&](const double* tot) { epi.finish(tot); });
     }
 }
@@ -995,9 +995,10 @@ __global__ void __launch_bounds__(256)
     constexpr int U = 8;
     __shared__ double red_sh[32 * NV];
     if (epi.skip()) return;
-    double acc[NV];
+    if constexpr (Epi::NV > 0) red_begin<NV>();
+    RAcc acc[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    for (int i = 0; i < NV; ++i) racc_zero(acc[i]);
     for (long long rr = blockIdx.x * (long long)blockDim.x + threadIdx.x; rr < nrows;
          rr += (long long)gridDim.x * blockDim.x) {
         const int r = static_cast<int>(rr);
@@ -1035,8 +1036,7 @@ __global__ void __launch_bounds__(256)
         epi.row(r, sum, acc);
     }
     if constexpr (Epi::NV > 0) {
-        block_sum<NV>(acc, threadIdx.x, blockDim.x, red_sh);
-        grid_reduce_finish<NV>(acc, ws, threadIdx.x, blockDim.x, red_sh,
+        grid_reduce<NV>(acc, ws, threadIdx.x, blockDim.x, red_sh,
                                [&](const double* tot) { epi.finish(tot); });
     }
 }
@@ -1052,9 +1052,10 @@ __global__ void __launch_bounds__(256)
     constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
     __shared__ double red_sh[32 * NV];
     if (epi.skip()) return;
-    double acc[NV];
+    if constexpr (Epi::NV > 0) red_begin<NV>();
+    RAcc acc[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    for (int i = 0; i < NV; ++i) racc_zero(acc[i]);
     for (long long rr = blockIdx.x * (long long)blockDim.x + threadIdx.x; rr < nrows;
          rr += (long long)gridDim.x * blockDim.x) {
         const int r = static_cast<int>(rr);
@@ -1079,8 +1080,7 @@ __global__ void __launch_bounds__(256)
         epi.row(r, sum, acc);
     }
     if constexpr (Epi::NV > 0) {
-        block_sum<NV>(acc, threadIdx.x, blockDim.x, red_sh);
-        grid_reduce_finish<NV>(acc, ws, threadIdx.x, blockDim.x, red_sh,
+        grid_reduce<NV>(acc, ws, threadIdx.x, blockDim.x, red_sh,
                                [&](const double* tot) { epi.finish(tot); });
     }
 }

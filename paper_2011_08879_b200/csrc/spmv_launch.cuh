@@ -3,6 +3,7 @@
 // (spmv.cu) and the fused solver steps (solver.cu).
 #pragma once
 
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 
@@ -74,9 +75,10 @@ __global__ void __launch_bounds__(256)
     constexpr int NV = Epi::NV > 0 ? Epi::NV : 1;
     __shared__ double red_sh[32 * NV];
     if (epi.skip()) return;
-    double acc[NV];
+    if constexpr (Epi::NV > 0) red_begin<NV>();
+    RAcc acc[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    for (int i = 0; i < NV; ++i) racc_zero(acc[i]);
     const int lane = threadIdx.x & 31;
     const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -100,8 +102,7 @@ __global__ void __launch_bounds__(256)
         if (lane == 0) epi.row(r, part, acc);
     }
     if constexpr (Epi::NV > 0) {
-        block_sum<NV>(acc, threadIdx.x, blockDim.x, red_sh);
-        grid_reduce_finish<NV>(acc, ws, threadIdx.x, blockDim.x, red_sh,
+        grid_reduce<NV>(acc, ws, threadIdx.x, blockDim.x, red_sh,
                                [&](const double* tot) { epi.finish(tot); });
     }
 }
@@ -160,6 +161,19 @@ void set_smem(K kernel, size_t bytes)
                                   static_cast<int>(bytes)));
 }
 
+// The >48 KB dynamic shared-memory opt-in is a per-device setting: `mask`
+// (one static per kernel instantiation at the call site) records the
+// devices this process has opted in on, so a second GPU driven from the
+// same process (second ctx, thread or peer group) opts in too.
+template <typename K>
+void smem_optin(std::atomic<unsigned long long>& mask, int device, K kernel, size_t bytes)
+{
+    const unsigned long long bit = 1ull << (device & 63);
+    if (mask.load(std::memory_order_acquire) & bit) return;
+    set_smem(kernel, bytes);
+    mask.fetch_or(bit, std::memory_order_acq_rel);
+}
+
 // Persistent grid: as many CTAs as fit (shared-memory bound), one warp per
 // tile at a time.
 template <typename T, int NIDX, int G, class K, class View, class Epi>
@@ -167,8 +181,8 @@ void stream_launch(lbk_ctx ctx, K kernel, const View& A, const T* x, const Epi& 
 {
     using Cfg = StreamCfg<T, NIDX>;
     constexpr size_t smem = Cfg::smem_bytes;
-    static bool attr = (set_smem(kernel, smem), true);
-    (void)attr;
+    static std::atomic<unsigned long long> optin{0};
+    smem_optin(optin, ctx->device, kernel, smem);
     static int bps = blocks_per_sm(kernel, Cfg::kThreads, smem);
     long long cap = static_cast<long long>(ctx->num_sms) * bps;
     if (cap > kRedMaxBlocks) cap = kRedMaxBlocks;
@@ -231,8 +245,8 @@ void launch_sellp_stream(lbk_ctx ctx, SellpView<T> A, const int* plan, int ntile
     using Cfg = StreamCfg<T, 1>;
     auto kernel = sellp_stream_kernel<T, Epi>;
     constexpr size_t smem = Cfg::smem_bytes;
-    static bool attr = (set_smem(kernel, smem), true);
-    (void)attr;
+    static std::atomic<unsigned long long> optin{0};
+    smem_optin(optin, ctx->device, kernel, smem);
     static int bps = blocks_per_sm(kernel, Cfg::kThreads, smem);
     long long cap = static_cast<long long>(ctx->num_sms) * bps;
     if (cap > kRedMaxBlocks) cap = kRedMaxBlocks;

@@ -70,6 +70,27 @@ def main():
     comm.sync(EX)
     out["spmv_back_to_back"] = all(
         np.array_equal(ys[k].cpu().numpy(), O.spmv_csr(A, xs[k])[lo:hi]) for k in range(5))
+    # two matrices with different neighbour sets on ONE communicator, applied
+    # A, B, B, A (B = diagonal: no halo at all) -- ADVICE r1: the per-
+    # communicator halo epoch advanced on B while only A's peers handed back
+    A = O.stencil("7pt", 12)
+    rk, world = dist.get_rank(), dist.get_world_size()
+    rp, cols, _ = D.local_rows(A.row_ptr, A.cols, A.vals, world, rk)
+    mA = D.DistMap(A.nrows, world, rk, rp, cols)
+    D.exchange_requests(mA)
+    shared = D.Communicator.peer(0, D.peer_halo_cap(mA))
+    KEEP.append(shared)
+    Bm = O.Csr(A.nrows, A.ncols, np.arange(A.nrows + 1, dtype=np.int32),
+               np.arange(A.nrows, dtype=np.int32), np.full(A.nrows, 2.0))
+    MA, _, lo, hi = setup(A, shared)
+    MB, _, _, _ = setup(Bm, shared)
+    xg = O.seeded_values(A.ncols, 31)
+    ok = True
+    for M, ref in ((MA, O.spmv_csr(A, xg)), (MB, 2.0 * xg), (MB, 2.0 * xg), (MA, O.spmv_csr(A, xg))):
+        y = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+        M.spmv(shared, M.ext_vector(xg[lo:hi]), y)
+        ok = ok and bool(np.array_equal(y.cpu().numpy(), ref[lo:hi]))
+    out["shared_comm_abba"] = ok
     # allreduce
     t = torch.tensor([float(dist.get_rank() + 1), 0.25], dtype=torch.float64, device="cuda")
     comm.allreduce_sum(EX, t)

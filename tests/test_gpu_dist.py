@@ -22,7 +22,7 @@ from conftest import relerr
 pytestmark = pytest.mark.gpu
 
 
-def build(O, lk, A, P, comm_kind="threads"):
+def build(O, lk, A, P):
     from paper_2011_08879_b200 import dist as D
     maps, parts = [], []
     for rank in range(P):
@@ -32,11 +32,7 @@ def build(O, lk, A, P, comm_kind="threads"):
     D.exchange_requests_local(maps)
     exs = [lk.CudaExecutor(0, stream=torch.cuda.Stream()) for _ in range(P)]
     mats = [D.DistCsrMatrix(exs[r], maps[r], parts[r][0], parts[r][1], A.nnz) for r in range(P)]
-    if comm_kind == "peer":
-        cap = max(m.halo_count() for m in maps)
-        comms = D.Communicator.peer_group([0] * P, cap)
-    else:
-        comms = D.Communicator.threads(P) if P > 1 else [None]
+    comms = D.Communicator.threads(P) if P > 1 else [None]
     return exs, mats, comms
 
 
@@ -219,6 +215,7 @@ def test_peer_spmv_bitexact(peer_run):
     for o in out:
         assert o["spmv_7pt"] and o["spmv_27pt"] and o["spmv_5pt"]
         assert o["spmv_back_to_back"]
+        assert o["shared_comm_abba"]
         assert o["allreduce"] == [P * (P + 1) / 2, 0.25 * P]
 
 

@@ -1,0 +1,128 @@
+"""GPU: full-size parity of the Krylov configs (cfg4 CG, cfg5 BiCGSTAB, 256^3)
+on one GPU and row-partitioned over P = 2, 4, 8 ranks.
+
+Two goldens, both generated on the CPU and committed:
+* tests/golden/cfg45.npz -- the REFERENCE LIBRARY (oracle/_ref,
+  ReferenceExecutor, krylov.cpp:119-230); the north-star bands hold against
+  it (CG 581 +-1 and every history entry within 1e-7;
+  BiCGSTAB in the reference's own spread [495, 498], the 1e-6 crossing at
+  275, the first 40 entries within 1e-6, final <= 1e-8);
+* tests/golden/cfg45_exact.npz -- krylov.cpp with exactly rounded dots
+  (oracle/xkrylov.cpp, the product's reduction): the GPU reproduces its
+  history, flop count and x (SHA-256) BIT FOR BIT -- on one GPU and at
+  every rank count, which is what makes the iteration count independent
+  of the partition."""
+import hashlib
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(os.path.join(GOLD, "cfg45.npz")), np.load(os.path.join(GOLD, "cfg45_exact.npz"))
+
+
+def check_cg(hist, iters, flops, gold):
+    ref, ex = gold
+    assert abs(iters - int(ref["cg_iters"])) <= 1
+    h = np.asarray(hist)
+    rh = ref["cg_hist"]
+    k = min(len(h), len(rh))
+    assert np.max(np.abs(h[:k] - rh[:k]) / rh[:k]) <= 1e-7
+    assert h[-1] <= 1e-8
+    assert iters == int(ex["cg_iters"]) and flops == int(ex["cg_flops"])
+    assert h.tolist() == ex["cg_hist"].tolist()  # bit for bit
+
+
+def check_bicg(hist, iters, flops, gold):
+    ref, ex = gold
+    assert 495 <= iters <= 498  # the reference's own executor spread
+    h = np.asarray(hist)
+    assert int(np.argmax(h <= 1e-6)) == 275
+    rh = ref["bicg_hist"]
+    assert np.max(np.abs(h[:41] - rh[:41]) / rh[:41]) <= 1e-6
+    assert h[-1] <= 1e-8
+    assert iters == int(ex["bicg_iters"]) and flops == int(ex["bicg_flops"])
+    assert h.tolist() == ex["bicg_hist"].tolist()  # bit for bit
+
+
+def sha(x):
+    return hashlib.sha256(np.ascontiguousarray(x, np.float64).tobytes()).hexdigest()
+
+
+def test_cfg4_cg_single_gpu(lk, ex, gold):
+    from paper_2011_08879_b200 import gen
+    A = gen.stencil(ex, "7pt", 256)
+    b = lk.make_vector(ex, A.nrows)
+    lk.spmv(A, lk.vector_from(ex, np.ones(A.ncols)), b)
+    x = lk.zeros(ex, A.nrows)
+    r = lk.solve(A, b, x, lk.SolverConfig(kind="cg", rel_tol=1e-8, max_iters=20000))
+    check_cg(r.residual_history, r.iterations, r.flop_count, gold)
+    assert sha(lk.vector_to_host(x)) == str(gold[1]["cg_x_sha256"])
+    # residual_mode 'recurrence' stops at the same iteration
+    r2 = lk.solve(A, b, lk.zeros(ex, A.nrows),
+                  lk.SolverConfig(kind="cg", rel_tol=1e-8, max_iters=20000,
+                                  residual_mode="recurrence"))
+    assert r2.iterations == r.iterations and r2.final_rel_residual == r.final_rel_residual
+
+
+def test_cfg5_bicgstab_single_gpu(lk, ex, gold):
+    from paper_2011_08879_b200 import gen
+    A = gen.stencil(ex, "7pt", 256, 0.5)
+    b = lk.make_vector(ex, A.nrows)
+    lk.spmv(A, lk.vector_from(ex, gen.seeded_values(A.ncols, 11)), b)
+    x = lk.zeros(ex, A.nrows)
+    r = lk.solve(A, b, x, lk.SolverConfig(kind="bicgstab", rel_tol=1e-8, max_iters=20000))
+    check_bicg(r.residual_history, r.iterations, r.flop_count, gold)
+    assert sha(lk.vector_to_host(x)) == str(gold[1]["bicg_x_sha256"])
+
+
+def _run_peer(P, cases, tmp):
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = []
+    for r in range(P):
+        env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(r),
+                   WORLD_SIZE=str(P), LBK_PEER_TIMEOUT="300")
+        procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests",
+                                                                     "peer_worker_full.py"),
+                                       str(tmp), ",".join(cases)], env=env))
+    try:
+        codes = [p.wait(timeout=1500) for p in procs]
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    assert codes == [0] * P, codes
+    return [json.loads((tmp / f"r{r}.json").read_text()) for r in range(P)]
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_full_size_distributed(P, gold, tmp_path):
+    """cfg4 CG (both residual modes) and cfg5 BiCGSTAB over P peer-memory
+    ranks: every rank reports the single-GPU golden bits; the assembled x
+    hashes to the golden."""
+    cases = ["cg", "bicgstab", "cg_rec"]
+    out = _run_peer(P, cases, tmp_path)
+    for o in out:
+        check_cg(o["cg"]["hist"], o["cg"]["iters"], o["cg"]["flops"], gold)
+        check_bicg(o["bicgstab"]["hist"], o["bicgstab"]["iters"], o["bicgstab"]["flops"], gold)
+        assert o["cg_rec"]["iters"] == o["cg"]["iters"]
+        assert o["cg_rec"]["hist"] == out[0]["cg_rec"]["hist"]
+    for case, key in (("cg", "cg_x_sha256"), ("bicgstab", "bicg_x_sha256")):
+        x = np.concatenate([np.load(tmp_path / f"r{r}_{case}.npy") for r in range(P)])
+        assert sha(x) == str(gold[1][key]), case

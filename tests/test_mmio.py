@@ -38,6 +38,8 @@ GOOD = {
 3 3 0
 """,
     "crlf_and_spaces": "%%MatrixMarket matrix coordinate real general\r\n2 2 2\r\n  1   1   3.0  \r\n2 2 4\r\n",
+    "crlf_comments": "%%MatrixMarket matrix coordinate real general\r\n% c\r\n%\r\n2 2 1\r\n1 1 3.0\r\n",
+    "crlf_pattern": "%%MatrixMarket matrix coordinate pattern general\r\n2 2 1\r\n1 1\r\n",
 }
 
 BAD = {
@@ -54,6 +56,11 @@ BAD = {
     "truncated": "%%MatrixMarket matrix coordinate real general\n2 2 3\n1 1 1.0\n",
     "negative": "%%MatrixMarket matrix coordinate real general\n-2 2 0\n",
     "empty_file": "",
+    # a CRLF blank line is "\r" to std::getline: not empty, so the reference
+    # parses it as the size / an entry line and fails
+    "crlf_blank_before_size": "%%MatrixMarket matrix coordinate real general\r\n\r\n2 2 1\r\n1 1 3.0\r\n",
+    "crlf_blank_between": "%%MatrixMarket matrix coordinate real general\r\n2 2 2\r\n1 1 3.0\r\n\r\n2 2 4\r\n",
+    "cr_only": "%%MatrixMarket matrix coordinate real general\r2 2 1\r1 1 3.0\r",
 }
 
 
@@ -66,8 +73,6 @@ def _write(tmp_path, name, text):
 @pytest.mark.parametrize("name", sorted(GOOD))
 def test_parse_matches_reference(R, tmp_path, name):
     O = R
-    if "crlf" in name:
-        pytest.skip("the reference's getline keeps '\\r'; our reader strips it (documented leniency)")
     path = _write(tmp_path, name, GOOD[name])
     nr, nc, rows, cols, vals = O.ref_read_mm(path)
     mr, mc, er, ec, ev = lk.read_matrix_market_entries(path)
@@ -124,3 +129,13 @@ def test_device_read_matches_reference(R, ex, tmp_path, name):
     assert np.array_equal(M.row_idx.cpu().numpy(), rows)
     assert np.array_equal(M.col_idx.cpu().numpy(), cols)
     assert np.array_equal(M.vals.cpu().numpy(), vals)
+
+
+def test_hostile_nnz_header(tmp_path):
+    """an nnz near INT64_MAX in the size line (symmetric: 2*nnz
+    would overflow) is a FormatError from the short entry list, not an
+    exception escaping the C ABI."""
+    path = _write(tmp_path, "huge", "%%MatrixMarket matrix coordinate real symmetric\n"
+                  "2 2 9223372036854775000\n1 1 1.0\n")
+    with pytest.raises(lk.FormatError):
+        lk.read_matrix_market_entries(path)

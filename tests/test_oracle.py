@@ -264,3 +264,62 @@ def test_full_size_goldens_committed():
     assert int(g["bicg_iters"]) == 495
     assert abs(g["bicg_hist"][1] - 1.136784e-01) <= 1e-6
     assert int(g["bicg_flops"]) == 495 * (6 * nnz + 28 * n) + 2 * nnz + 2 * n
+
+
+# ------------------------------------------ exactly rounded reductions
+def test_xdot_pinned_to_fsum(O):
+    """oracle/xkrylov.cpp's exact dot == Python's math.fsum (an independent
+    exactly rounded sum) on wide-range, cancelling and subnormal data."""
+    import math
+    rng = np.random.default_rng(5)
+    for n in (1, 17, 5000, 70000):
+        for scale in (0, 200, 300):
+            x = rng.standard_normal(n) * 10.0 ** rng.integers(-scale, scale + 1, n)
+            y = rng.standard_normal(n)
+            assert O.xdot(x, y) == math.fsum((x * y).tolist())
+    h = rng.standard_normal(1001)
+    v = np.concatenate([h, -h, [1e-300]])
+    assert O.xsum(v) == math.fsum(v.tolist()) == 1e-300
+    t = rng.standard_normal(3000) * 1e-160
+    assert O.xsum(t * t) == math.fsum((t * t).tolist())
+
+
+@pytest.mark.parametrize("kind,m,gamma", [("cg", 16, 0.0), ("cg", 32, 0.0),
+                                          ("bicgstab", 24, 0.5)])
+def test_xsolve_restates_krylov(O, kind, m, gamma):
+    """The exact-dot restatement of krylov.cpp agrees with the reference
+    library (sequential dots) to rounding: same iterations (the reference's
+    own spread for BiCGSTAB), histories within the §8c bands over the first
+    40 iterations, same flop accounting."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    A = O.stencil("7pt", m, gamma)
+    xs = np.ones(A.nrows) if kind == "cg" else O.seeded_values(A.nrows, 11)
+    b = O.spmv_csr(A, xs)
+    r = O.xsolve(A, b, kind, tol=1e-8, max_iters=5000)
+    rr = O.ref_solve(A, b, kind, rel_tol=1e-8, max_iters=5000)
+    rp = O.ref_solve(A, b, kind, rel_tol=1e-8, max_iters=5000, exec_kind=1, workers=8)
+    assert abs(r["iterations"] - rr.iterations) <= max(1, abs(rp.iterations - rr.iterations))
+    k = min(len(r["history"]), len(rr.history), 40)
+    h, g = r["history"][:k], np.asarray(rr.history[:k])
+    # SURVEY.md §8c bands: CG 1e-7; BiCGSTAB (chaotic under rounding) 1e-6
+    assert np.max(np.abs(h - g) / g) <= (1e-7 if kind == "cg" else 1e-6)
+    if r["iterations"] == rr.iterations:
+        assert r["flops"] == rr.flop_count
+    if kind == "cg":
+        assert r["iterations"] == {16: 41, 32: 81}[m]  # SURVEY.md §8c goldens
+
+
+def test_cfg45_exact_golden_is_consistent(O):
+    """The committed full-size exact-dot goldens satisfy the north-star
+    bands against the reference library's full-size goldens."""
+    import os
+    ref = np.load(os.path.join(os.path.dirname(__file__), "golden", "cfg45.npz"))
+    ex = np.load(os.path.join(os.path.dirname(__file__), "golden", "cfg45_exact.npz"))
+    assert int(ex["cg_iters"]) == int(ref["cg_iters"]) == 581
+    assert np.max(np.abs(ex["cg_hist"] - ref["cg_hist"]) / ref["cg_hist"]) <= 1e-7
+    assert int(ex["cg_flops"]) == int(ref["cg_flops"])
+    assert 495 <= int(ex["bicg_iters"]) <= 498
+    assert int(np.argmax(ex["bicg_hist"] <= 1e-6)) == 275
+    assert np.max(np.abs(ex["bicg_hist"][:41] - ref["bicg_hist"][:41]) / ref["bicg_hist"][:41]) <= 1e-6
+    assert ex["bicg_hist"][-1] <= 1e-8
