@@ -44,16 +44,43 @@ __global__ void fill_kernel(long long n, double v, double* __restrict__ x)
         x[i] = v;
 }
 
-__global__ void dot_kernel(long long n, const double* __restrict__ x,
+__global__ void __launch_bounds__(256, 3) dot_kernel(long long n, const double* __restrict__ x,
                            const double* __restrict__ y, RedWs ws, int take_sqrt)
 {
     __shared__ double sh[32];
     red_begin<1>();
     RAcc acc[1];
     racc_zero(acc[0]);
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
-        racc_add(acc, 0, mul_rn(x[i], y[i]));
+    // the adds of one step's terms run after the next step's loads issue
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    double pend[4] = {0.0, 0.0, 0.0, 0.0};
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n;
+         i0 += 4 * stride) {
+        double t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long i = i0 + u * stride;
+            t[u] = i < n ? mul_rn(x[i], y[i]) : 0.0;
+        }
+#pragma unroll 1
+        for (int u = 0; u < 4; ++u) {  // one xl_add instance: small code
+            racc_add(acc, 0, pend[0]);
+            pend[0] = pend[1];
+            pend[1] = pend[2];
+            pend[2] = pend[3];
+            pend[3] = t[0];
+            t[0] = t[1];
+            t[1] = t[2];
+            t[2] = t[3];
+        }
+    }
+#pragma unroll 1
+    for (int u = 0; u < 4; ++u) {
+        racc_add(acc, 0, pend[0]);
+        pend[0] = pend[1];
+        pend[1] = pend[2];
+        pend[2] = pend[3];
+    }
     grid_reduce<1>(acc, ws, threadIdx.x, blockDim.x, sh, [&](const double* t) {
         ws.out[0] = take_sqrt ? sqrt(t[0]) : t[0];
     });

@@ -116,11 +116,11 @@ struct MappedEpi {
         const int m = __ldg(map + r);
         return {m, EpiPre<Epi>::load(e, m)};
     }
-    __device__ void row_pre(int, double s, const Pre& p, RAcc* acc) const
+    __device__ void row_pre(int, double s, const Pre& p, auto* acc) const
     {
         EpiPre<Epi>::row(e, p.r, s, p.p, acc);
     }
-    __device__ void row(int r, double s, RAcc* acc) const { e.row(__ldg(map + r), s, acc); }
+    __device__ void row(int r, double s, auto* acc) const { e.row(__ldg(map + r), s, acc); }
     __device__ void finish(const double* t) const { e.finish(t); }
 };
 
@@ -131,7 +131,7 @@ struct OffsetEpiBase {
     int off;
     __device__ bool skip() const { return e.skip(); }
     __device__ void prefetch(int rb, int re) const { EpiPf<Epi>::run(e, rb + off, re + off); }
-    __device__ void row(int r, double s, RAcc* acc) const { e.row(r + off, s, acc); }
+    __device__ void row(int r, double s, auto* acc) const { e.row(r + off, s, acc); }
     __device__ void finish(const double* t) const { e.finish(t); }
 };
 template <class Epi, class = void>
@@ -141,7 +141,7 @@ template <class Epi>
 struct OffsetEpi<Epi, std::void_t<typename Epi::Pre>> : OffsetEpiBase<Epi> {
     using Pre = typename Epi::Pre;
     __device__ Pre pre(int r) const { return this->e.pre(r + this->off); }
-    __device__ void row_pre(int r, double s, const Pre& p, RAcc* acc) const
+    __device__ void row_pre(int r, double s, const Pre& p, auto* acc) const
     {
         this->e.row_pre(r + this->off, s, p, acc);
     }

@@ -234,9 +234,35 @@ using RAcc = XLane;
 __device__ __forceinline__ void racc_zero(RAcc& a) { xl_zero(a); }
 __device__ __forceinline__ void racc_add(RAcc* acc, int k, double t)
 {
-    xl_add(acc[k], t, g_xsh + k * kXV);
+    xl_add(acc[k], t, xwarp_limbs() + k * kXV);
 }
 #endif
+
+// One element's (row's) terms, buffered so that their exact adds can run
+// off the critical path: after the next element's / pass's loads are issued
+// (vec_kernel, staged_rows).  Every epilogue / vec op adds at most one term
+// per value and element.
+template <int NV>
+struct Terms {
+    double v[NV > 0 ? NV : 1];
+};
+template <int NV>
+__device__ __forceinline__ void racc_add(Terms<NV>* t, int k, double x)
+{
+    t->v[k] = x;
+}
+template <int NV>
+__device__ __forceinline__ void terms_zero(Terms<NV>& t)
+{
+#pragma unroll
+    for (int k = 0; k < (NV > 0 ? NV : 1); ++k) t.v[k] = 0.0;
+}
+template <int NV>
+__device__ __forceinline__ void terms_flush(RAcc* acc, const Terms<NV>& t)
+{
+#pragma unroll
+    for (int k = 0; k < NV; ++k) racc_add(acc, k, t.v[k]);
+}
 
 // Kernel prologue of every reducing kernel (all threads, after any
 // block-uniform early exit): zeroes the block accumulator.
@@ -324,11 +350,13 @@ __device__ __forceinline__ bool grid_reduce(RAcc (&acc)[NV], RedWs ws, int tid, 
         return grid_reduce_finish<NV>(acc, ws, tid, nthreads, sh, fin);
     } else {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) xl_warp_flush(acc[v], g_xsh + v * kXV);
+        for (int v = 0; v < NV; ++v) xl_warp_flush(acc[v], xwarp_limbs() + v * kXV);
         __syncthreads();
         long long* G = ws.defer ? ws.xout : ws.xacc;
+        const int nw = (nthreads + 31) >> 5;
         for (int i = tid; i < NV * kXV; i += nthreads) {
-            const long long v = g_xsh[i];
+            long long v = 0;
+            for (int w = 0; w < nw; ++w) v += g_xsh[w * kXSlot + i];
             if (v) atomicAdd(reinterpret_cast<unsigned long long*>(G + i),
                              static_cast<unsigned long long>(v));
         }

@@ -126,8 +126,8 @@ struct EpiInit {
         l2_prefetch_rows(b, rb, re);
     }
     __device__ Pre pre(int i) const { return {b[i]}; }
-    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
+    __device__ void row(int i, double s, auto* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, auto* acc) const
     {
         const double v = add_rn(pr.b, -s);
         r[i] = v;
@@ -175,8 +175,8 @@ struct EpiCgK1 {
         double p;
     };
     __device__ Pre pre(int i) const { return {p[i]}; }
-    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
+    __device__ void row(int i, double s, auto* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, auto* acc) const
     {
         q[i] = s;
         racc_add(acc, 0, mul_rn(pr.p, s));
@@ -213,8 +213,8 @@ struct EpiCgK3 {
         double b, p, r;
     };
     __device__ Pre pre(int i) const { return {b[i], p[i], r[i]}; }
-    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
+    __device__ void row(int i, double s, auto* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, auto* acc) const
     {
         const double t = add_rn(pr.b, -s);
         racc_add(acc, 0, mul_rn(t, t));
@@ -271,8 +271,8 @@ struct EpiTrueRes {
         l2_prefetch_rows(b, rb, re);
     }
     __device__ Pre pre(int i) const { return {b[i]}; }
-    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int, double s, const Pre& pr, RAcc* acc) const
+    __device__ void row(int i, double s, auto* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int, double s, const Pre& pr, auto* acc) const
     {
         const double t = add_rn(pr.b, -s);
         racc_add(acc, 0, mul_rn(t, t));
@@ -319,8 +319,8 @@ struct EpiBiB2 {
         l2_prefetch_rows(rt, rb, re);
     }
     __device__ Pre pre(int i) const { return {rt[i]}; }
-    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
+    __device__ void row(int i, double s, auto* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, auto* acc) const
     {
         v[i] = s;
         racc_add(acc, 0, mul_rn(pr.rt, s));
@@ -352,8 +352,8 @@ struct EpiBiB4 {
         l2_prefetch_rows(s, rb, re);
     }
     __device__ Pre pre(int i) const { return {s[i]}; }
-    __device__ void row(int i, double sum, RAcc* acc) const { row_pre(i, sum, pre(i), acc); }
-    __device__ void row_pre(int i, double sum, const Pre& pr, RAcc* acc) const
+    __device__ void row(int i, double sum, auto* acc) const { row_pre(i, sum, pre(i), acc); }
+    __device__ void row_pre(int i, double sum, const Pre& pr, auto* acc) const
     {
         t[i] = sum;
         racc_add(acc, 0, mul_rn(sum, sum));
@@ -396,8 +396,8 @@ struct EpiBiB6 {
         l2_prefetch_rows(r, rb, re);
     }
     __device__ Pre pre(int i) const { return {b[i], p[i], v[i], r[i]}; }
-    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
+    __device__ void row(int i, double s, auto* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, auto* acc) const
     {
         const double t = add_rn(pr.b, -s);
         racc_add(acc, 0, mul_rn(t, t));
@@ -461,8 +461,8 @@ struct EpiCgsV {
         l2_prefetch_rows(rt, rb, re);
     }
     __device__ Pre pre(int i) const { return {rt[i]}; }
-    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
+    __device__ void row(int i, double s, auto* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, auto* acc) const
     {
         v[i] = s;
         racc_add(acc, 0, mul_rn(pr.rt, s));
@@ -499,8 +499,8 @@ struct EpiCgsT {
         l2_prefetch_rows(rt, rb, re);
     }
     __device__ Pre pre(int i) const { return {x[i], r[i], w[i], rt[i]}; }
-    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
+    __device__ void row(int i, double s, auto* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, auto* acc) const
     {
         const double a = st->alpha;
         t[i] = s;
@@ -530,8 +530,8 @@ struct EpiCgsRes {
         l2_prefetch_rows(b, rb, re);
     }
     __device__ Pre pre(int i) const { return {b[i]}; }
-    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int, double s, const Pre& pr, RAcc* acc) const
+    __device__ void row(int i, double s, auto* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int, double s, const Pre& pr, auto* acc) const
     {
         const double t = add_rn(pr.b, -s);
         racc_add(acc, 0, mul_rn(t, t));
@@ -599,8 +599,8 @@ struct EpiGmRes {
         l2_prefetch_rows(b, rb, re);
     }
     __device__ Pre pre(int i) const { return {b[i]}; }
-    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
+    __device__ void row(int i, double s, auto* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, auto* acc) const
     {
         const double t = add_rn(pr.b, -s);
         v0[i] = t;
@@ -678,8 +678,8 @@ struct EpiGmApply {
         l2_prefetch_rows(v0, rb, re);
     }
     __device__ Pre pre(int i) const { return {v0[i]}; }
-    __device__ void row(int i, double s, RAcc* acc) const { row_pre(i, s, pre(i), acc); }
-    __device__ void row_pre(int i, double s, const Pre& pr, RAcc* acc) const
+    __device__ void row(int i, double s, auto* acc) const { row_pre(i, s, pre(i), acc); }
+    __device__ void row_pre(int i, double s, const Pre& pr, auto* acc) const
     {
         w[i] = s;
         racc_add(acc, 0, mul_rn(pr.v0, s));
@@ -702,8 +702,10 @@ template <class Op>
 struct NoFinish<Op, std::void_t<decltype(Op::kNoFinish)>> : std::bool_constant<Op::kNoFinish> {
 };
 
+// >= 4 CTAs (32 warps) per SM: a streaming pass needs the loads of many
+// warps in flight; the exact accumulator must not cost occupancy
 template <class Op>
-__global__ void __launch_bounds__(256) vec_kernel(long long n, Op op, RedWs ws)
+__global__ void __launch_bounds__(256, 4) vec_kernel(long long n, Op op, RedWs ws)
 {
     pdl_enter();
     constexpr int NV = Op::NV;
@@ -714,9 +716,55 @@ __global__ void __launch_bounds__(256) vec_kernel(long long n, Op op, RedWs ws)
 #pragma unroll
     for (int i = 0; i < NV; ++i) racc_zero(acc[i]);
     op.prologue();
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
-        op.elem(i, acc);
+    // U elements per step (4, or 2 for ops with many operands: the 64-
+    // register budget of 4 CTAs/SM): all loads of the step first (ahead of
+    // any store, so nothing serialises on possible aliasing), then the
+    // updates; the exact adds of a step's terms run during the NEXT step,
+    // after its loads are issued (software-pipelined like staged_rows), from
+    // one non-unrolled loop so the kernel keeps one xl_add instance
+    constexpr int U = sizeof(typename Op::In) <= 16 ? 4 : 2;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    Terms<NV> pend[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) terms_zero(pend[u]);
+    long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    for (; i0 + (U - 1) * stride < n; i0 += U * stride) {
+        typename Op::In in[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) in[u] = op.load(i0 + u * stride);
+        Terms<NV> t[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            terms_zero(t[u]);
+            op.elem(i0 + u * stride, in[u], &t[u]);
+        }
+        if constexpr (!NoFinish<Op>::value) {
+#pragma unroll 1
+            for (int u = 0; u < U; ++u) {
+                terms_flush(acc, pend[0]);
+#pragma unroll
+                for (int k = 0; k + 1 < U; ++k) pend[k] = pend[k + 1];
+                pend[U - 1] = t[0];
+#pragma unroll
+                for (int k = 0; k + 1 < U; ++k) t[k] = t[k + 1];
+            }
+        }
+    }
+    for (; i0 < n; i0 += stride) {  // the last < U elements
+        const typename Op::In in = op.load(i0);
+        Terms<NV> t;
+        terms_zero(t);
+        op.elem(i0, in, &t);
+        if constexpr (!NoFinish<Op>::value) terms_flush(acc, t);
+    }
+    if constexpr (!NoFinish<Op>::value) {
+#pragma unroll 1
+        for (int u = 0; u < U; ++u) {
+            terms_flush(acc, pend[0]);
+#pragma unroll
+            for (int k = 0; k + 1 < U; ++k) pend[k] = pend[k + 1];
+        }
+    }
     if constexpr (!NoFinish<Op>::value) {
         grid_reduce<NV>(acc, ws, threadIdx.x, blockDim.x, sh,
                                [&](const double* tot) { op.finish(tot); });
@@ -735,10 +783,14 @@ struct OpCgK2 {
     double alpha;
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     __device__ void prologue() { alpha = st->alpha; }
-    __device__ void elem(long long i, RAcc* acc) const
+    struct In {
+        double x, p, r, q;
+    };
+    __device__ In load(long long i) const { return {x[i], p[i], r[i], q[i]}; }
+    __device__ void elem(long long i, const In& in, auto* acc) const
     {
-        x[i] = add_rn(x[i], mul_rn(alpha, p[i]));
-        const double rn = add_rn(r[i], mul_rn(-alpha, q[i]));
+        x[i] = add_rn(in.x, mul_rn(alpha, in.p));
+        const double rn = add_rn(in.r, mul_rn(-alpha, in.q));
         r[i] = rn;
         racc_add(acc, 0, mul_rn(rn, rn));
     }
@@ -778,7 +830,14 @@ struct OpCgP {
     double beta;
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     __device__ void prologue() { beta = st->beta; }
-    __device__ void elem(long long i, RAcc*) const { p[i] = add_rn(mul_rn(p[i], beta), r[i]); }
+    struct In {
+        double p, r;
+    };
+    __device__ In load(long long i) const { return {p[i], r[i]}; }
+    __device__ void elem(long long i, const In& in, auto*) const
+    {
+        p[i] = add_rn(mul_rn(in.p, beta), in.r);
+    }
     static constexpr bool kNoFinish = true;  // nothing to reduce
     __device__ void finish(const double*) const {}
 };
@@ -793,9 +852,13 @@ struct OpBiB3 {
     double alpha;
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     __device__ void prologue() { alpha = st->alpha; }
-    __device__ void elem(long long i, RAcc* acc) const
+    struct In {
+        double r, v;
+    };
+    __device__ In load(long long i) const { return {r[i], v[i]}; }
+    __device__ void elem(long long i, const In& in, auto* acc) const
     {
-        const double sv = add_rn(r[i], mul_rn(-alpha, v[i]));
+        const double sv = add_rn(in.r, mul_rn(-alpha, in.v));
         s[i] = sv;
         racc_add(acc, 0, mul_rn(sv, sv));
     }
@@ -823,13 +886,16 @@ struct OpBiB5 {
         alpha = st->alpha;
         omega = st->omega;
     }
-    __device__ void elem(long long i, RAcc* acc) const
+    struct In {
+        double s, x, p, t, rt;
+    };
+    __device__ In load(long long i) const { return {s[i], x[i], p[i], t[i], rt[i]}; }
+    __device__ void elem(long long i, const In& in, auto* acc) const
     {
-        const double si = s[i];
-        x[i] = add_rn(add_rn(x[i], mul_rn(alpha, p[i])), mul_rn(omega, si));
-        const double rn = add_rn(si, mul_rn(-omega, t[i]));
+        x[i] = add_rn(add_rn(in.x, mul_rn(alpha, in.p)), mul_rn(omega, in.s));
+        const double rn = add_rn(in.s, mul_rn(-omega, in.t));
         r[i] = rn;
-        racc_add(acc, 0, mul_rn(rt[i], rn));
+        racc_add(acc, 0, mul_rn(in.rt, rn));
     }
     __device__ void finish(const double* tot) const
     {
@@ -856,12 +922,15 @@ struct OpCgsUP {
         return *(volatile int*)&st->done != 0 || *(volatile int*)&st->iter <= 1;
     }
     __device__ void prologue() { beta = st->beta; }
-    __device__ void elem(long long i, RAcc*) const
+    struct In {
+        double q, r, p;
+    };
+    __device__ In load(long long i) const { return {q[i], r[i], p[i]}; }
+    __device__ void elem(long long i, const In& in, auto*) const
     {
-        const double qi = q[i];
-        const double ui = add_rn(mul_rn(qi, beta), r[i]);
+        const double ui = add_rn(mul_rn(in.q, beta), in.r);
         u[i] = ui;
-        p[i] = add_rn(mul_rn(add_rn(mul_rn(p[i], beta), qi), beta), ui);
+        p[i] = add_rn(mul_rn(add_rn(mul_rn(in.p, beta), in.q), beta), ui);
     }
     // nothing to reduce: the distributed path skips the rank exchange
     static constexpr bool kNoFinish = true;
@@ -879,12 +948,15 @@ struct OpCgsQW {
     double alpha;
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     __device__ void prologue() { alpha = st->alpha; }
-    __device__ void elem(long long i, RAcc*) const
+    struct In {
+        double u, v;
+    };
+    __device__ In load(long long i) const { return {u[i], v[i]}; }
+    __device__ void elem(long long i, const In& in, auto*) const
     {
-        const double ui = u[i];
-        const double qi = add_rn(ui, mul_rn(-alpha, v[i]));
+        const double qi = add_rn(in.u, mul_rn(-alpha, in.v));
         q[i] = qi;
-        w[i] = add_rn(ui, qi);
+        w[i] = add_rn(in.u, qi);
     }
     static constexpr bool kNoFinish = true;  // nothing to reduce
     __device__ void finish(const double*) const {}
@@ -903,11 +975,15 @@ struct OpGmMgs {
     double h;
     __device__ bool skip() const { return gm_step_skip(st, jj); }
     __device__ void prologue() { h = st->gm->H[(i - 1) * st->gm->restart + jj]; }
-    __device__ void elem(long long k, RAcc* acc) const
+    struct In {
+        double w, vprev, vi;
+    };
+    __device__ In load(long long k) const { return {w[k], vprev[k], vi ? vi[k] : 0.0}; }
+    __device__ void elem(long long k, const In& in, auto* acc) const
     {
-        const double wn = add_rn(w[k], mul_rn(-h, vprev[k]));
+        const double wn = add_rn(in.w, mul_rn(-h, in.vprev));
         w[k] = wn;
-        racc_add(acc, 0, mul_rn(vi ? vi[k] : wn, wn));
+        racc_add(acc, 0, mul_rn(vi ? in.vi : wn, wn));
     }
     __device__ void finish(const double* tot) const
     {
@@ -960,7 +1036,11 @@ struct OpGmScale {
     double inv;
     __device__ bool skip() const { return gm_step_skip(st, jj); }
     __device__ void prologue() { inv = 1.0 / (w ? st->gm->hnext : st->gm->beta); }
-    __device__ void elem(long long k, RAcc*) const { v[k] = mul_rn(w ? w[k] : v[k], inv); }
+    struct In {
+        double a;
+    };
+    __device__ In load(long long k) const { return {w ? w[k] : v[k]}; }
+    __device__ void elem(long long k, const In& in, auto*) const { v[k] = mul_rn(in.a, inv); }
     static constexpr bool kNoFinish = true;  // nothing to reduce
     __device__ void finish(const double*) const {}
 };
@@ -993,14 +1073,18 @@ struct OpGmUpdate {
     int steps;
     __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
     __device__ void prologue() { steps = st->gm->steps; }
-    __device__ void elem(long long k, RAcc*) const
+    struct In {};
+    __device__ In load(long long) const { return {}; }
+    __device__ void elem(long long k, const In&, auto*) const
     {
         const double* y = st->gm->y;
         double v = x[k];
         for (int i = 0; i < steps; ++i) v = add_rn(v, mul_rn(__ldg(y + i), V[i * ld + k]));
         x[k] = v;
     }
-    __device__ void finish(const double*) const { st->flops += 2LL * steps * st->n; }
+    // reads the step count from the state: in the distributed environment
+    // finish() runs in a separate kernel on a copy whose prologue never ran
+    __device__ void finish(const double*) const { st->flops += 2LL * st->gm->steps * st->n; }
 };
 
 // -------------------------------------------------------- operators
@@ -1316,7 +1400,14 @@ struct OpSelfDot {
     const double* __restrict__ b;
     __device__ bool skip() const { return false; }
     __device__ void prologue() {}
-    __device__ void elem(long long i, RAcc* acc) const { racc_add(acc, 0, mul_rn(b[i], b[i])); }
+    struct In {
+        double b;
+    };
+    __device__ In load(long long i) const { return {b[i]}; }
+    __device__ void elem(long long, const In& in, auto* acc) const
+    {
+        racc_add(acc, 0, mul_rn(in.b, in.b));
+    }
     __device__ void finish(const double*) const {}
 };
 struct EpiSqrtTot {
@@ -1832,3 +1923,17 @@ lbk_status lbk_dist_solve(lbk_ctx ctx, lbk_dist_csr D, lbk_comm comm, const doub
 }
 
 }  // extern "C"
+
+#ifdef LBK_XRED_STATS
+// dev builds only (scripts/variants.sh LBK_XRED_STATS): exact-reduction
+// lane statistics of the solver kernels {flushes, slides, re-centres, -}
+extern "C" int lbk_dbg_xred_stats(unsigned long long* out, int reset)
+{
+    cudaMemcpyFromSymbol(out, lbk::g_xred_stats, sizeof(unsigned long long) * 4);
+    if (reset) {
+        unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbol(lbk::g_xred_stats, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

@@ -71,7 +71,7 @@ struct EpiStore {
     static constexpr int NV = 0;
     T* __restrict__ y;
     __device__ bool skip() const { return false; }
-    __device__ void row(int r, T s, RAcc*) const { y[r] = s; }
+    __device__ void row(int r, T s, auto*) const { y[r] = s; }
     __device__ void finish(const double*) const {}
 };
 
@@ -90,13 +90,13 @@ struct EpiAxpby {
             if (beta != T(0)) l2_prefetch_rows(reinterpret_cast<const double*>(y), rb, re);
     }
     __device__ Pre pre(int r) const { return {beta != T(0) ? y[r] : T(0)}; }
-    __device__ void row_pre(int r, T s, const Pre& p, RAcc*) const
+    __device__ void row_pre(int r, T s, const Pre& p, auto*) const
     {
         T v = mul_rn(alpha, s);
         if (beta != T(0)) v = add_rn(v, mul_rn(beta, p.y));
         y[r] = v;
     }
-    __device__ void row(int r, T s, RAcc* acc) const { row_pre(r, s, pre(r), acc); }
+    __device__ void row(int r, T s, auto* acc) const { row_pre(r, s, pre(r), acc); }
     __device__ void finish(const double*) const {}
 };
 
@@ -253,7 +253,7 @@ struct EpiPre {
     struct type {};
     __device__ static type load(const Epi&, int) { return {}; }
     template <typename T>
-    __device__ static void row(const Epi& e, int r, T s, const type&, RAcc* acc)
+    __device__ static void row(const Epi& e, int r, T s, const type&, auto* acc)
     {
         e.row(r, s, acc);
     }
@@ -264,7 +264,7 @@ struct EpiPre<Epi, std::void_t<typename Epi::Pre>> {
     using type = typename Epi::Pre;
     __device__ static type load(const Epi& e, int r) { return e.pre(r); }
     template <typename T>
-    __device__ static void row(const Epi& e, int r, T s, const type& p, RAcc* acc)
+    __device__ static void row(const Epi& e, int r, T s, const type& p, auto* acc)
     {
         e.row_pre(r, s, p, acc);
     }
@@ -302,12 +302,20 @@ constexpr int kSeqRow = 256;  // staged rows up to this length stay bit-exact
 // base + q*32 + lane starts (the tile's entry end for rows >= re); a row's
 // extent is then its start and the next row's start, taken from the
 // neighbouring lane -- one lookup per row instead of two.
+//
+// Exact reductions (xred.cuh): the terms of a pass's rows go to `pend` and
+// are added into the lane accumulator during the NEXT pass, right after its
+// gathers are issued -- the adds overlap the gather latency instead of
+// lengthening the pass.  The caller flushes `pend` at the end.
 template <typename T, int G, class Epi, class Starts>
 __device__ __forceinline__ void staged_rows(int rb, int re, T* sv, const int* sc,
                                             const T* __restrict__ x, const Epi& epi,
-                                            RAcc* acc, Starts&& starts)
+                                            RAcc* acc, Terms<Epi::NV>* pend, Starts&& starts)
 {
     using EP = EpiPre<Epi>;
+    // (NV == 1 only: two values' pending terms cost 2G registers that the
+    // 255-register sweep does not have -- B4 spilled)
+    constexpr bool kPipe = kExactRed && Epi::NV == 1;
     constexpr int CH = 32 / G;
     const int lane = threadIdx.x & 31;
     for (int base = rb; base < re; base += 32 * G) {
@@ -349,16 +357,31 @@ __device__ __forceinline__ void staged_rows(int rb, int re, T* sv, const int* sc
             }
 #pragma unroll
             for (int q = 0; q < G; ++q) {
+                if constexpr (kPipe) {  // the previous pass's terms, under the gathers
+                    terms_flush(acc, pend[q]);
+                    terms_zero(pend[q]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
                 const int r = base + q * 32 + lane;
                 if (r < re) {
                     T sum = T(0);
 #pragma unroll
                     for (int j = 0; j < CH; ++j)
                         if (j < len[q]) sum = add_rn(sum, mul_rn(v[q][j], g[q][j]));
-                    EP::row(epi, r, sum, pre[q], acc);
+                    if constexpr (kPipe) EP::row(epi, r, sum, pre[q], &pend[q]);
+                    else EP::row(epi, r, sum, pre[q], acc);
                 }
             }
             continue;
+        }
+        if constexpr (kPipe) {
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+                terms_flush(acc, pend[q]);
+                terms_zero(pend[q]);
+            }
         }
         // products of the pass's whole entry span, in place
         const int lo = __shfl_sync(0xffffffffu, o[0], 0);
@@ -576,6 +599,9 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
     RAcc acc[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) racc_zero(acc[i]);
+    Terms<Epi::NV> pend[G];  // exact mode: the last pass's terms (staged_rows)
+#pragma unroll
+    for (int q = 0; q < G; ++q) terms_zero(pend[q]);
 
     struct RowPf {
         int v[G + 1];
@@ -604,7 +630,7 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
             return int4x2{make_int4(bd.x, bd.y - 1, bd.z, ks), make_int4(bd.y - 1, bd.y, ks, bd.w)};
         },
         [&](int4 bd, int ka, T* sv, const int* sc, const int*, const RowPf& p) {
-            staged_rows<T, G>(bd.x, bd.y, sv, sc, x, epi, acc, [&](int base, int* st) {
+            staged_rows<T, G>(bd.x, bd.y, sv, sc, x, epi, acc, pend, [&](int base, int* st) {
                 if (base == bd.x) {  // prefetched when the tile was staged
 #pragma unroll
                     for (int q = 0; q <= G; ++q) st[q] = p.v[q] - ka;
@@ -626,6 +652,10 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
         },
         [&](int4 bd) { EpiPf<Epi>::run(epi, bd.x, bd.y); });
 
+    if constexpr (kExactRed && Epi::NV == 1) {
+#pragma unroll
+        for (int q = 0; q < G; ++q) terms_flush(acc, pend[q]);
+    }
     if constexpr (Epi::NV > 0) {
         __syncthreads();
         grid_reduce<NV>(acc, ws, tid, Cfg::kThreads, red_sh,
@@ -764,6 +794,9 @@ __global__ void __launch_bounds__((StreamCfg<T, 2>::kThreads), 2)
     RAcc acc[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) racc_zero(acc[i]);
+    Terms<Epi::NV> pend[G];  // exact mode: the last pass's terms (staged_rows)
+#pragma unroll
+    for (int q = 0; q < G; ++q) terms_zero(pend[q]);
 
     struct NoPf {};
     warp_tile_loop<T, 2>(
@@ -790,7 +823,7 @@ __global__ void __launch_bounds__((StreamCfg<T, 2>::kThreads), 2)
         },
         [&](int4 bd, int ka, T* sv, const int* sc, const int* sr, const NoPf&) {
             const int lo = bd.z - ka, hi = bd.w - ka;
-            staged_rows<T, G>(bd.x, bd.y, sv, sc, x, epi, acc, [&](int base, int* st) {
+            staged_rows<T, G>(bd.x, bd.y, sv, sc, x, epi, acc, pend, [&](int base, int* st) {
 #pragma unroll
                 for (int q = 0; q < G; ++q) {
                     const int r = base + q * 32 + lane;
@@ -817,6 +850,10 @@ __global__ void __launch_bounds__((StreamCfg<T, 2>::kThreads), 2)
         },
         [&](int4 bd) { EpiPf<Epi>::run(epi, bd.x, bd.y); });
 
+    if constexpr (kExactRed && Epi::NV == 1) {
+#pragma unroll
+        for (int q = 0; q < G; ++q) terms_flush(acc, pend[q]);
+    }
     if constexpr (Epi::NV > 0) {
         __syncthreads();
         grid_reduce<NV>(acc, ws, tid, Cfg::kThreads, red_sh,

@@ -41,9 +41,15 @@ constexpr int kXV = 80;           // int64 per reduced value (padded)
 constexpr int kXMaxNV = 2;        // values per fused reduction
 constexpr int kXSlot = kXMaxNV * kXV;  // int64 per reduction slot
 
-// Block accumulator: NV values x kXV limbs.  One per CTA, shared by every
-// kernel of a translation unit that reduces (zeroed by xred_begin).
-static __shared__ long long g_xsh[kXSlot];
+// Block accumulator: one region of NV values x kXV limbs per warp (lanes
+// flush into their own warp's region, so warps never contend), shared by
+// every kernel of a translation unit that reduces (zeroed by xred_begin).
+constexpr int kXWarps = 8;  // reducing kernels run <= 256 threads
+static __shared__ long long g_xsh[kXWarps * kXSlot];
+__device__ __forceinline__ long long* xwarp_limbs()
+{
+    return g_xsh + (threadIdx.x >> 5) * kXSlot;
+}
 
 struct XLane {
     unsigned long long w0, w1, w2;
@@ -74,7 +80,7 @@ __device__ __forceinline__ void sub192(XLane& a, unsigned long long t0, unsigned
 
 // Flush one lane's window into a value's limbs (shared or global) with
 // atomics.  Window value = U - neg * 2^192 at limb `base`.
-static __device__ __noinline__ void xl_flush_atomic(const XLane& a, long long* limbs)
+__device__ __forceinline__ void xl_flush_atomic(const XLane& a, long long* limbs)
 {
     if ((a.w0 | a.w1 | a.w2) == 0) return;
     const unsigned long long w[3] = {a.w0, a.w1, a.w2};
@@ -94,60 +100,17 @@ static __device__ __noinline__ void xl_special(double v, long long* limbs)
     atomicAdd(reinterpret_cast<unsigned long long*>(limbs + which), 1ull);
 }
 
-// Add one term.  `limbs` = this value's block accumulator (flush target).
-__device__ __forceinline__ void xl_add(XLane& a, double v, long long* limbs)
-{
-    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
-    if ((bits << 1) == 0) return;  // +-0
-    const int e = static_cast<int>((bits >> 52) & 0x7ff);
-    if (e == 0x7ff) {
-        xl_special(v, limbs);
-        return;
-    }
-    const unsigned long long m = (bits & 0xfffffffffffffull) | (e ? (1ull << 52) : 0ull);
-    const int pos = e ? e - 1 : 0;  // bit position of m's lsb
-    int s = pos - 32 * a.base;
-    if (static_cast<unsigned>(s) > 107u) {  // outside the window (or empty)
-        xl_flush_atomic(a, limbs);
-        const int b = (pos >> 5) - 1;
-        a.base = b < 0 ? 0 : b;
-        a.w0 = a.w1 = a.w2 = 0;
-        s = pos - 32 * a.base;
-    }
-    unsigned long long t0, t1, t2;
-    if (s < 64) {
-        t0 = m << s;
-        t1 = s ? (m >> (64 - s)) : 0ull;
-        t2 = 0;
-    } else {
-        const int u = s - 64;
-        t0 = 0;
-        t1 = m << u;
-        t2 = u ? (m >> (64 - u)) : 0ull;
-    }
-    if (bits >> 63) sub192(a, t0, t1, t2);
-    else add192(a, t0, t1, t2);
-}
-
-// Zero the block accumulator; every thread of the block must call.
-template <int NV>
-__device__ __forceinline__ void xred_begin()
-{
-    for (int i = threadIdx.x; i < NV * kXV; i += blockDim.x) g_xsh[i] = 0;
-    __syncthreads();
-}
-
 // Warp-aggregated flush of every lane's window into the block limbs
 // (all 32 lanes call).  When the lanes' windows lie within 2 limbs of each
 // other (the normal case) the warp adds them with redux.sync on 16-bit
 // halves and lane 0 posts 9 limbs; otherwise every lane flushes itself.
-__device__ __forceinline__ void xl_warp_flush(const XLane& a, long long* limbs)
+__device__ __forceinline__ void xl_group_flush(const XLane& a, long long* limbs, unsigned mask)
 {
     const bool nz = (a.w0 | a.w1 | a.w2) != 0;
-    const unsigned act = __ballot_sync(0xffffffffu, nz);
+    const unsigned act = __ballot_sync(mask, nz);
     if (!act) return;
-    const int lo = __reduce_min_sync(0xffffffffu, nz ? a.base : 0x7fffffff);
-    const int hi = __reduce_max_sync(0xffffffffu, nz ? a.base : -0x7fffffff);
+    const int lo = __reduce_min_sync(mask, nz ? a.base : 0x7fffffff);
+    const int hi = __reduce_max_sync(mask, nz ? a.base : -0x7fffffff);
     if (hi - lo > 2) {
         xl_flush_atomic(a, limbs);
         return;
@@ -174,15 +137,15 @@ __device__ __forceinline__ void xl_warp_flush(const XLane& a, long long* limbs)
     // sign: the shifted 256-bit value stands for V + neg * 2^(256) at limb
     // lo; the top 2*sh digits of the shifted-out part are all sign bits
     const int neg = nz && (a.w2 >> 63);
-    const int nneg = __popc(__ballot_sync(0xffffffffu, neg));
+    const int nneg = __popc(__ballot_sync(mask, neg));
     long long tot[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        const unsigned l16 = __reduce_add_sync(0xffffffffu, dd[k] & 0xffffu);
-        const unsigned h16 = __reduce_add_sync(0xffffffffu, dd[k] >> 16);
+        const unsigned l16 = __reduce_add_sync(mask, dd[k] & 0xffffu);
+        const unsigned h16 = __reduce_add_sync(mask, dd[k] >> 16);
         tot[k] = static_cast<long long>(l16) + (static_cast<long long>(h16) << 16);
     }
-    if ((threadIdx.x & 31) == 0) {
+    if ((threadIdx.x & 31) == __ffs(mask) - 1) {
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             if (tot[k])
@@ -192,6 +155,93 @@ __device__ __forceinline__ void xl_warp_flush(const XLane& a, long long* limbs)
             atomicAdd(reinterpret_cast<unsigned long long*>(limbs + lo + 8),
                       static_cast<unsigned long long>(-static_cast<long long>(nneg)));
     }
+}
+
+__device__ __forceinline__ void xl_warp_flush(const XLane& a, long long* limbs)
+{
+    xl_group_flush(a, limbs, 0xffffffffu);
+}
+
+#ifdef LBK_XRED_STATS
+static __device__ unsigned long long g_xred_stats[4];  // direct terms, -, placements, -
+#define LBK_XSTAT(i) atomicAdd(&g_xred_stats[i], 1ull)
+#else
+#define LBK_XSTAT(i) ((void)0)
+#endif
+
+// A term outside the lane's window goes straight into the warp's limbs:
+// its three 32-bit digits, added (or, negative, subtracted) with shared-
+// memory atomics.  No re-centring, no warp vote, no call -- small code on
+// the cold path, and the window keeps serving the common magnitudes.
+__device__ __forceinline__ void xl_direct(unsigned long long m, int pos, bool neg,
+                                          long long* limbs)
+{
+    const int li = pos >> 5, off = pos & 31;
+    const unsigned long long lo = m << off;                 // digits 0, 1
+    const unsigned long long d2 = off ? (m >> (64 - off)) : 0ull;  // digit 2
+    const long long d0 = static_cast<long long>(lo & 0xffffffffull);
+    const long long d1 = static_cast<long long>(lo >> 32);
+    const long long sg = neg ? -1 : 1;
+    auto* L = reinterpret_cast<unsigned long long*>(limbs + li);
+    if (d0) atomicAdd(L, static_cast<unsigned long long>(sg * d0));
+    if (d1) atomicAdd(L + 1, static_cast<unsigned long long>(sg * d1));
+    if (d2) atomicAdd(L + 2, static_cast<unsigned long long>(sg * static_cast<long long>(d2)));
+    LBK_XSTAT(0);
+}
+
+// Add one term.  `limbs` = this value's flush target (the warp's limbs).
+__device__ __forceinline__ void xl_add(XLane& a, double v, long long* limbs)
+{
+    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
+    if ((bits << 1) == 0) return;  // +-0
+    const int e = static_cast<int>((bits >> 52) & 0x7ff);
+    if (e == 0x7ff) {
+        xl_special(v, limbs);
+        return;
+    }
+    const unsigned long long m = (bits & 0xfffffffffffffull) | (e ? (1ull << 52) : 0ull);
+    const int pos = e ? e - 1 : 0;  // bit position of m's lsb
+    int s = pos - 32 * a.base;
+    if (__builtin_expect(static_cast<unsigned>(s) > 107u, 0)) {  // outside the window
+        if (s < 0) {  // far below the largest terms so far: straight to the limbs
+            xl_direct(m, pos, bits >> 63, limbs);
+            return;
+        }
+        // above the window (or the lane's first term): the window follows
+        // the largest magnitude -- flush it exactly and re-place it with
+        // this term's lsb 64..95 bits above the bottom (room for terms up
+        // to 2^64 smaller, and for 12..43 bits of growth); bounded by the
+        // ~65 limbs of the double range per lane
+        xl_flush_atomic(a, limbs);
+        const int b = (pos >> 5) - 2;
+        a.base = b < 0 ? 0 : b;
+        a.w0 = a.w1 = a.w2 = 0;
+        s = pos - 32 * a.base;
+        LBK_XSTAT(2);
+    }
+    // m << s over 192 bits, two's-complement negated for a negative term:
+    // (t ^ sg) + (sg & 1) -- branch-free, carried into the 192-bit add
+    const bool hi = s >= 64;
+    const int u = hi ? s - 64 : s;
+    const unsigned long long lo_w = m << u;
+    const unsigned long long hi_w = u ? (m >> (64 - u)) : 0ull;
+    const unsigned long long sg = static_cast<unsigned long long>(static_cast<long long>(bits) >> 63);
+    const unsigned long long t0 = (hi ? 0ull : lo_w) ^ sg;
+    const unsigned long long t1 = (hi ? lo_w : hi_w) ^ sg;
+    const unsigned long long t2 = (hi ? hi_w : 0ull) ^ sg;
+    asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u64 %2, %2, %5;\n\t"
+        "add.cc.u64 %0, %0, %6;\n\taddc.cc.u64 %1, %1, 0;\n\taddc.u64 %2, %2, 0;"
+        : "+l"(a.w0), "+l"(a.w1), "+l"(a.w2)
+        : "l"(t0), "l"(t1), "l"(t2), "l"(sg & 1ull));
+}
+
+// Zero the block accumulator; every thread of the block must call.
+template <int NV>
+__device__ __forceinline__ void xred_begin()
+{
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int i = threadIdx.x; i < nw * kXSlot; i += blockDim.x) g_xsh[i] = 0;
+    __syncthreads();
 }
 
 // Round a value's limbs to the nearest double (ties to even), in place
