@@ -312,7 +312,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "steps": K, "warmup": args.warmup, "ms_per_step": elapsed_max / K * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (App. B 27-pt stencil generated on device; x = seeded_values(n, 11))",
-        "config": dict(WORKLOAD, parallelism=f"replicas x{world}"),
+        "config": WORKLOAD,
+        "parallelism": f"replicas x{world}",
         "gflops": round(world * 2 * nnz * K / elapsed_max / 1e9, 1),
         "roofline": {"bound": "hbm", "kernel": "csr_stream_kernel", "achieved": round(achieved, 1),
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s",
@@ -348,9 +349,42 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                 f.write(R.emit_report(recs, fmt))
 
 
-def time_launches(ex, call, steps: int, warmup: int) -> float:
+def cfg3_check(rp, ci, va, xh, y_csr, y_coo) -> dict:
+    """cfg3 output check (measured but never verified): CSR and
+    COO y agree bit for bit on every row of <= 256 entries and normwise
+    everywhere, and a 65,536-row sample matches a host recomputation in the
+    reference's order (sum from 0.0 in ascending k, reference.cpp:82-88)
+    within 1e-12 normwise (bit-exact for rows <= 256)."""
+    import numpy as np
+    yc, yo = y_csr.cpu().numpy(), y_coo.cpu().numpy()
+    lens = np.diff(rp.astype(np.int64))
+    short = lens <= 256
+    rng = np.random.default_rng(3)
+    rows = np.sort(rng.choice(len(lens), 65536, replace=False))
+    ref = np.empty(rows.size)
+    for i, r in enumerate(rows):  # sequential sums: the reference's bits
+        s = 0.0
+        for k in range(int(rp[r]), int(rp[r + 1])):
+            s += va[k] * xh[ci[k]]
+        ref[i] = s
+    d = np.abs(yc[rows] - ref).max() / max(np.abs(ref).max(), 1e-300)
+    sh = short[rows]
+    out = {"rows": int(len(lens)), "nnz": int(rp[-1]), "max_row": int(lens.max()),
+           "csr_eq_coo_rows_le_256": bool(np.array_equal(yc[short], yo[short])),
+           "csr_vs_coo_normwise": float(np.abs(yc - yo).max() / np.abs(yc).max()),
+           "sample_rows": int(rows.size), "sample_normwise_vs_host": float(d),
+           "sample_bitexact_rows_le_256": bool(np.array_equal(yc[rows][sh], ref[sh]))}
+    out["ok"] = (out["csr_eq_coo_rows_le_256"] and out["sample_bitexact_rows_le_256"]
+                 and out["sample_normwise_vs_host"] <= 1e-12 and out["csr_vs_coo_normwise"] <= 1e-12)
+    if not out["ok"]:
+        print(f"bench: cfg3 check FAILED {out}", file=sys.stderr)
+    return out
+
+
+def time_launches(ex, call, steps: int, warmup: int, flush=None) -> float:
     """Mean device time of one launch (CUDA event pair per launch, launches
-    back to back on the executor's stream)."""
+    back to back on the executor's stream; with `flush`, that buffer is
+    rewritten before every launch, outside the event pair)."""
     import torch
     for _ in range(warmup):
         call()
@@ -358,6 +392,9 @@ def time_launches(ex, call, steps: int, warmup: int) -> float:
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(steps)]
     for a, b in evs:
+        if flush is not None:
+            with torch.cuda.stream(ex.stream):
+                flush.fill_(1)
         a.record(ex.stream)
         call()
         b.record(ex.stream)
@@ -377,7 +414,7 @@ def run_formats(ex, lib, A, x, y, steps: int, warmup: int, no_cfg3: bool) -> dic
     peak, _ = measured_peak()
     out = {"peak_gbs": peak, "note": "GB/s = algorithmic bytes / mean launch time"}
 
-    def meas(key, M, xv, yv, nbytes, nnz):
+    def meas(key, M, xv, yv, nbytes, nnz, flush=None):
         fn = {lk.CsrMatrix: "csr", lk.CooMatrix: "coo", lk.EllMatrix: "ell",
               lk.SellpMatrix: "sellp"}[type(M)]
         fn = getattr(lib, f"lbk_spmv_{fn}_{'f32' if xv.values.dtype == torch.float32 else 'f64'}")
@@ -388,7 +425,7 @@ def run_formats(ex, lib, A, x, y, steps: int, warmup: int, no_cfg3: bool) -> dic
             st = fn(ex.ctx, C.byref(d), xp, yp)
             if st:
                 lk._check(st, ex.ctx)
-        t = time_launches(ex, call, max(steps, 10), max(warmup, 3))
+        t = time_launches(ex, call, max(steps, 10), max(warmup, 3), flush)
         out[key] = {"us": round(t * 1e6, 2), "gbs": round(nbytes / t / 1e9, 1),
                     "gflops": round(2 * nnz / t / 1e9, 1), "frac": round(nbytes / t / 1e9 / peak, 3),
                     "bytes": int(nbytes), "nnz": int(nnz)}
@@ -468,20 +505,28 @@ def run_formats(ex, lib, A, x, y, steps: int, warmup: int, no_cfg3: bool) -> dic
     x1 = lk.vector_from(ex, gen.seeded_values(A1.ncols, 11))
     y1 = lk.make_vector(ex, A1.nrows)
     n1, z1 = A1.nrows, A1.nnz()
-    meas("cfg1_csr_f64", A1, x1, y1, 12 * z1 + 4 * (n1 + 1) + 16 * n1, z1)
+    # cfg1's 84 MB fit in the 126 MB L2: flush it between launches (a 512 MB
+    # write outside the timed event pair), SURVEY.md §8d
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=ex.device)
+    meas("cfg1_csr_f64", A1, x1, y1, 12 * z1 + 4 * (n1 + 1) + 16 * n1, z1, flush=flush)
+    out["cfg1_csr_f64"]["l2"] = "flushed (512 MB write) before every timed launch"
+    del flush
     del A1
     if not no_cfg3:
         nn = 1 << 24
         rp, ci, va = gen.powerlaw_host(nn)
         A3 = lk.csr_from_host(ex, nn, nn, rp, ci, va)
-        del rp, ci, va
         z3 = A3.nnz()
-        x3 = lk.vector_from(ex, gen.seeded_values(nn, 11))
+        x3h = gen.seeded_values(nn, 11)
+        x3 = lk.vector_from(ex, x3h)
         y3 = lk.make_vector(ex, nn)
         meas("cfg3_csr_f64", A3, x3, y3, 12 * z3 + 4 * (nn + 1) + 16 * nn, z3)
+        y_csr = y3.values.clone()
         C3 = lk.csr_to_coo(A3)
         meas("cfg3_coo_f64", C3, x3, y3, 16 * z3 + 16 * nn, z3)
         del C3
+        out["cfg3_check"] = cfg3_check(rp, ci, va, x3h, y_csr, y3.values)
+        del rp, ci, va, y_csr
         A3f = A3.astype(torch.float32)
         del A3
         x3f = lk.DenseVector(x3.values.float(), ex)
@@ -490,6 +535,15 @@ def run_formats(ex, lib, A, x, y, steps: int, warmup: int, no_cfg3: bool) -> dic
         del A3f
     torch.cuda.empty_cache()
     return out
+
+
+def band_check(iters: int) -> bool:
+    """cfg5 BiCGSTAB: the reference's own executor spread [495, 498]
+    (SURVEY.md §8c-note); a miss is reported on stderr and in the line."""
+    ok = 495 <= iters <= 498
+    if not ok:
+        print(f"bench: cfg5 BiCGSTAB {iters} iterations outside [495, 498]", file=sys.stderr)
+    return ok
 
 
 def run_cg(ex, world: int, rank: int, local_rank: int, force_dist: bool = False) -> dict:
@@ -545,6 +599,7 @@ def run_cg(ex, world: int, rank: int, local_rank: int, force_dist: bool = False)
         r = lk.solve(A5, b5, xs, lk.SolverConfig(kind="bicgstab", rel_tol=1e-8, max_iters=20000))
         cg["bicgstab_cfg5"] = {"config": "cfg5: 7-pt upwind gamma 0.5 256^3, b = A x*, tol 1e-8",
                                "golden_iterations": "495 (reference) / 498 (parallel)",
+                               "in_band": band_check(r.iterations),
                                "iterations": r.iterations,
                                "final_rel_residual": r.final_rel_residual, "seconds": r.elapsed,
                                "iters_per_s": r.iterations / r.elapsed,
@@ -667,6 +722,7 @@ def run_cg(ex, world: int, rank: int, local_rank: int, force_dist: bool = False)
     cg["bicgstab_cfg5"] = {"config": "cfg5: 7-pt upwind gamma 0.5 256^3, b = A x*, tol 1e-8, "
                                      f"row-partitioned over {world} GPUs",
                            "golden_iterations": "495 (reference) / 498 (parallel)",
+                           "in_band": band_check(r.iterations),
                            "iterations": r.iterations, "final_rel_residual": r.final_rel_residual,
                            "seconds": el, "iters_per_s": r.iterations / el,
                            "flop_count": r.flop_count,
@@ -681,20 +737,55 @@ def _cfg2_host():
     return O, O.stencil("27pt", 128)
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline_sample(reps: int = 5) -> dict:
-    """The reference library (oracle/_ref) on this host's cores: median of
-    `reps` cfg2 CSR SpMVs with ParallelExecutor(nproc)."""
+    """The reference library (oracle/_ref) on this host (CPU
+    timing beside it): cfg2 CSR SpMV with ParallelExecutor(nproc) (the
+    `value`, median of `reps`) and ReferenceExecutor (1 core, median of 3);
+    the reference's own host stream-copy peak (measure_peak_bandwidth,
+    harness.cpp:125-141) on both executors; and cfg4 CG seconds per
+    iteration at fixed_iters = 50 (krylov.hpp:30) on ParallelExecutor(nproc).
+    About 15 s of host work."""
     try:
         O, A = _cfg2_host()
         if not O.ref_available():
             raise RuntimeError("oracle/_ref not built")
         cores = os.cpu_count() or 1
         x = O.seeded_values(A.ncols, 11)
+        b2 = csr_bytes(A.nrows, A.ncols, A.nnz)
         _, med = O.ref_spmv(A, x, "csr", exec_kind=O.EXEC_PARALLEL, workers=cores, reps=reps)
-        return {"value": round(csr_bytes(A.nrows, A.ncols, A.nnz) / med / 1e9, 3), "unit": "GB/s",
-                "cores": cores, "kind": "reference",
-                "sample": f"cfg2 CSR SpMV, reference ParallelExecutor({cores}), median of {reps}",
-                "ms_per_step": med * 1e3}
+        _, med1 = O.ref_spmv(A, x, "csr", exec_kind=0, workers=1, reps=3)
+        out = {"value": round(b2 / med / 1e9, 3), "unit": "GB/s", "cores": cores,
+               "kind": "reference", "cpu_model": cpu_model(),
+               "sample": f"cfg2 CSR SpMV, reference ParallelExecutor({cores}), median of {reps}",
+               "ms_per_step": med * 1e3,
+               "reference_executor_1core": {"gbs": round(b2 / med1 / 1e9, 3),
+                                            "ms_per_step": med1 * 1e3,
+                                            "sample": "cfg2 CSR SpMV, ReferenceExecutor, median of 3"}}
+        del A
+        out["host_stream_copy_gbs"] = {
+            f"parallel({cores})": round(O.ref_peak_bandwidth(O.EXEC_PARALLEL, cores, 1 << 27, 3), 2),
+            "reference(1)": round(O.ref_peak_bandwidth(0, 1, 1 << 27, 3), 2),
+            "note": "the reference's measure_peak_bandwidth (harness.cpp:125-141), 128 MiB arrays"}
+        import numpy as np
+        A4 = O.stencil("7pt", 256)
+        b4 = O.spmv_csr(A4, np.ones(A4.nrows))
+        r = O.ref_solve(A4, b4, "cg", rel_tol=1e-8, fixed_iters=50, exec_kind=O.EXEC_PARALLEL,
+                        workers=cores)
+        out["cg_cfg4_fixed50"] = {"s_per_iter": r.elapsed / 50, "iters_per_s": 50 / r.elapsed,
+                                  "executor": f"ParallelExecutor({cores})",
+                                  "note": "reference solve(), fixed_iters = 50 (krylov.hpp:30)"}
+        return out
     except Exception as e:  # reported, never fatal for the GPU arm
         return {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
                 "sample": f"unavailable: {e}"}
@@ -723,7 +814,8 @@ def run_reference(args, rank: int) -> None:
             "ms_per_step": total / len(times) * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (App. B 27-pt stencil, oracle generator)",
-            "config": dict(WORKLOAD, parallelism=f"host ParallelExecutor({cores})"),
+            "config": WORKLOAD,
+            "parallelism": f"host ParallelExecutor({cores})", "cpu_model": cpu_model(),
             "gflops": round(2 * A.nnz * len(times) / total / 1e9, 3),
             "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "reference",
                              "sample": f"cfg2 CSR SpMV through the reference's spmv_csr, "

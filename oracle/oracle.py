@@ -115,6 +115,8 @@ def ref():
             "ref_csr_to_coo": (C.c_int, [C.c_int, C.c_int, i64, i32p, i32p, f64p, i32p, i32p, f64p]),
             "ref_validate": (C.c_int, [C.c_int, C.c_int, C.c_int, i64, i32p, i32p, f64p]),
             "ref_read_mm": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64), C.c_void_p, C.c_void_p, C.c_void_p]),
+            "ref_measure_peak_bandwidth": (C.c_int, [C.c_int, C.c_int, i64, C.c_int,
+                                                     C.POINTER(C.c_double)]),
             "ref_solve": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i64, i32p, i32p, f64p, f64p, f64p, C.c_int, C.c_double, C.c_int, C.c_int, f64p, C.c_int, i32p, f64p, C.POINTER(i64)]),
         }
         for name, (res, args) in sig.items():
@@ -414,3 +416,11 @@ def xsolve(a: Csr, b: np.ndarray, kind: str = "cg", x0=None, tol: float = 1e-8,
     return {"status": st, "iterations": it.value, "converged": bool(conv.value),
             "history": hist[: it.value + 1].copy(), "flops": fl.value,
             "breakdown_iter": bd.value, "x": x}
+
+
+def ref_peak_bandwidth(exec_kind: int = 1, workers: int = 1, bytes_: int = 1 << 27,
+                       reps: int = 3) -> float:
+    """The reference's measure_peak_bandwidth (harness.cpp:125-141), GB/s."""
+    out = C.c_double()
+    _chk(ref().ref_measure_peak_bandwidth(exec_kind, workers, bytes_, reps, C.byref(out)))
+    return out.value

@@ -26,6 +26,7 @@
 #include <string>
 #include <vector>
 
+#include "larch/bench/harness.hpp"
 #include "larch/core/error.hpp"
 #include "larch/core/executor.hpp"
 #include "larch/kernels/kernels.hpp"
@@ -361,6 +362,18 @@ int ref_solve(int exec_kind, int workers, int fmt, int kind, int n,
         auto m = std::min<std::size_t>(res.residual_history.size(),
                                        static_cast<std::size_t>(hist_cap));
         std::memcpy(hist, res.residual_history.data(), m * sizeof(double));
+    });
+}
+
+/// The reference's own host bandwidth calibration: measure_peak_bandwidth
+/// (harness.cpp:125-141) -- stream copy of `bytes` per array on the given
+/// executor, median of `reps`; GB/s to *out.
+int ref_measure_peak_bandwidth(int exec_kind, int workers, std::int64_t bytes, int reps,
+                               double* out)
+{
+    return guarded([&] {
+        auto exec = make_exec(exec_kind, workers);
+        *out = larch::measure_peak_bandwidth(exec, static_cast<std::size_t>(bytes), reps);  // GB/s (safe_rate)
     });
 }
 

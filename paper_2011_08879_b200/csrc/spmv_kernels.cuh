@@ -212,11 +212,17 @@ __device__ __forceinline__ T warp_row_global(int ks, int ke, const int* __restri
                                              const T* __restrict__ vals, const T* __restrict__ x)
 {
     const int lane = threadIdx.x & 31;
-    if (ke - ks <= 32) {
-        T p = T(0);
-        if (ks + lane < ke) p = mul_rn(__ldcs(vals + ks + lane), ldg_nc(x + __ldcs(cols + ks + lane)));
+    if (ke - ks <= 256) {
+        // up to kSeqRow entries (a row that overflowed its tile's slot can be
+        // this short): products 32 at a time, summed in ascending k through
+        // shuffles -- the reference's order and bits (reference.cpp:82-88)
         T sum = T(0);
-        for (int k = 0; k < ke - ks; ++k) sum = add_rn(sum, __shfl_sync(0xffffffffu, p, k));
+        for (int c = ks; c < ke; c += 32) {
+            T p = T(0);
+            if (c + lane < ke) p = mul_rn(__ldcs(vals + c + lane), ldg_nc(x + __ldcs(cols + c + lane)));
+            const int m = ke - c < 32 ? ke - c : 32;
+            for (int k = 0; k < m; ++k) sum = add_rn(sum, __shfl_sync(0xffffffffu, p, k));
+        }
         return sum;
     }
     // 16 independent loads (and then gathers) per lane in flight per round

@@ -126,3 +126,68 @@ def test_full_size_distributed(P, gold, tmp_path):
     for case, key in (("cg", "cg_x_sha256"), ("bicgstab", "bicg_x_sha256")):
         x = np.concatenate([np.load(tmp_path / f"r{r}_{case}.npy") for r in range(P)])
         assert sha(x) == str(gold[1][key]), case
+
+
+# ------------------------------------------------------------------ cfg3
+@pytest.fixture(scope="module")
+def cfg3(O):
+    """cfg3 at full size: the product's power-law generator (lbk_gen_powerlaw,
+    the one bench.py uses) next to the oracle's (port_powerlaw_new), both
+    SURVEY.md App. B (2^24 rows, window 65,536, max row 10,000)."""
+    from paper_2011_08879_b200 import gen
+    n = 1 << 24
+    rp, ci, va = gen.powerlaw_host(n)
+    R = O.powerlaw(n)
+    return n, rp, ci, va, R
+
+
+def test_cfg3_generator_matches_oracle(cfg3):
+    n, rp, ci, va, R = cfg3
+    assert int(rp[-1]) == R.nnz == 268_195_029  # App. B nnz KAT (SURVEY.md §8a)
+    assert int(np.diff(R.row_ptr).max()) == 10_000
+    assert np.array_equal(rp, R.row_ptr)
+    assert np.array_equal(ci, R.cols)
+    assert np.array_equal(va, R.vals)
+
+
+def test_cfg3_fp64_csr_coo_full(O, lk, ex, cfg3):
+    """FP64 CSR and COO SpMV on the full cfg3 matrix (16.7M rows, 268M nnz,
+    x of 128 MiB > L2, int32 offsets near 2^28): rows of <= 256 entries are
+    bit-identical to the reference order, the whole vector within 1e-12."""
+    from conftest import relerr
+    n, rp, ci, va, R = cfg3
+    xh = O.seeded_values(n, 11)
+    yref = O.spmv_csr(R, xh)
+    A = lk.csr_from_host(ex, n, n, rp, ci, va)
+    x = lk.vector_from(ex, xh)
+    short = np.diff(rp) <= 256
+    for name, M in (("csr", A), ("coo", lk.csr_to_coo(A))):
+        y = lk.make_vector(ex, n)
+        y.values.fill_(float("nan"))
+        lk.spmv(M, x, y)
+        yh = lk.vector_to_host(y)
+        assert relerr(yh, yref) <= 1e-12, name
+        assert np.array_equal(yh[short], yref[short]), name
+        del M, y
+
+
+def test_cfg3_fp32_csr_full(O, lk, ex, cfg3):
+    """FP32 CSR on the full cfg3 matrix: within 1e-5 of the FP64 product of
+    the FP32-rounded inputs; rows <= 256 equal the FP32 restatement."""
+    import torch
+    from conftest import relerr
+    n, rp, ci, va, R = cfg3
+    x32 = O.seeded_values(n, 11).astype(np.float32)
+    v32 = va.astype(np.float32)
+    ref64 = O.spmv_csr(O.Csr(n, n, R.row_ptr, R.cols, v32.astype(np.float64)),
+                       x32.astype(np.float64))
+    ref32 = O.spmv_csr(O.Csr(n, n, R.row_ptr, R.cols, v32), x32)
+    A = lk.csr_from_host(ex, n, n, rp, ci, v32, dtype=torch.float32)
+    x = lk.vector_from(ex, x32)
+    y = lk.make_vector(ex, n, torch.float32)
+    lk.spmv(A, x, y)
+    yh = lk.vector_to_host(y)
+    assert yh.dtype == np.float32
+    assert relerr(yh, ref64) <= 1e-5
+    short = np.diff(rp) <= 256
+    assert np.array_equal(yh[short], ref32[short])
