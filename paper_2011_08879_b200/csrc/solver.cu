@@ -720,8 +720,7 @@ __global__ void __launch_bounds__(256, 4) vec_kernel(long long n, Op op, RedWs w
     // register budget of 4 CTAs/SM): all loads of the step first (ahead of
     // any store, so nothing serialises on possible aliasing), then the
     // updates; the exact adds of a step's terms run during the NEXT step,
-    // after its loads are issued (software-pipelined like staged_rows), from
-    // one non-unrolled loop so the kernel keeps one xl_add instance
+    // after its loads are issued (software-pipelined like staged_rows)
     constexpr int U = sizeof(typename Op::In) <= 16 ? 4 : 2;
     const long long stride = (long long)gridDim.x * blockDim.x;
     Terms<NV> pend[U];
@@ -739,14 +738,10 @@ __global__ void __launch_bounds__(256, 4) vec_kernel(long long n, Op op, RedWs w
             op.elem(i0 + u * stride, in[u], &t[u]);
         }
         if constexpr (!NoFinish<Op>::value) {
-#pragma unroll 1
+#pragma unroll
             for (int u = 0; u < U; ++u) {
-                terms_flush(acc, pend[0]);
-#pragma unroll
-                for (int k = 0; k + 1 < U; ++k) pend[k] = pend[k + 1];
-                pend[U - 1] = t[0];
-#pragma unroll
-                for (int k = 0; k + 1 < U; ++k) t[k] = t[k + 1];
+                terms_flush(acc, pend[u]);
+                pend[u] = t[u];
             }
         }
     }

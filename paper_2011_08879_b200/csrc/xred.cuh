@@ -56,6 +56,20 @@ struct XLane {
     int base;  // window = limbs [base, base + 6)
 };
 
+// 64-bit add into a shared-memory limb with two native 32-bit atomics
+// (sm_100 has no shared 64-bit atomic add: atomicAdd(u64) on shared memory
+// compiles to a CAS spin loop).  The low word's carry comes from its own
+// atomic's old value, so the limb is exact once all adds have landed.
+__device__ __forceinline__ void smem_add64(long long* p, long long v)
+{
+    unsigned* w = reinterpret_cast<unsigned*>(p);
+    const unsigned lo = static_cast<unsigned>(v);
+    const unsigned hi = static_cast<unsigned>(static_cast<unsigned long long>(v) >> 32);
+    const unsigned old = atomicAdd(w, lo);
+    const unsigned h = hi + ((old + lo) < old ? 1u : 0u);
+    if (h) atomicAdd(w + 1, h);
+}
+
 __device__ __forceinline__ void xl_zero(XLane& a)
 {
     a.w0 = a.w1 = a.w2 = 0;
@@ -87,17 +101,16 @@ __device__ __forceinline__ void xl_flush_atomic(const XLane& a, long long* limbs
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
         const unsigned long long d = (w[k >> 1] >> (32 * (k & 1))) & 0xffffffffull;
-        if (d) atomicAdd(reinterpret_cast<unsigned long long*>(limbs + a.base + k), d);
+        if (d) smem_add64(limbs + a.base + k, static_cast<long long>(d));
     }
     if (a.w2 >> 63)
-        atomicAdd(reinterpret_cast<unsigned long long*>(limbs + a.base + 6),
-                  static_cast<unsigned long long>(-1LL));
+        smem_add64(limbs + a.base + 6, -1LL);
 }
 
 static __device__ __noinline__ void xl_special(double v, long long* limbs)
 {
     const int which = v != v ? kXNan : (v > 0 ? kXPinf : kXNinf);
-    atomicAdd(reinterpret_cast<unsigned long long*>(limbs + which), 1ull);
+    smem_add64(limbs + which, 1LL);
 }
 
 // Warp-aggregated flush of every lane's window into the block limbs
@@ -149,11 +162,9 @@ __device__ __forceinline__ void xl_group_flush(const XLane& a, long long* limbs,
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             if (tot[k])
-                atomicAdd(reinterpret_cast<unsigned long long*>(limbs + lo + k),
-                          static_cast<unsigned long long>(tot[k]));
+                smem_add64(limbs + lo + k, tot[k]);
         if (nneg)
-            atomicAdd(reinterpret_cast<unsigned long long*>(limbs + lo + 8),
-                      static_cast<unsigned long long>(-static_cast<long long>(nneg)));
+            smem_add64(limbs + lo + 8, -static_cast<long long>(nneg));
     }
 }
 
@@ -182,10 +193,10 @@ __device__ __forceinline__ void xl_direct(unsigned long long m, int pos, bool ne
     const long long d0 = static_cast<long long>(lo & 0xffffffffull);
     const long long d1 = static_cast<long long>(lo >> 32);
     const long long sg = neg ? -1 : 1;
-    auto* L = reinterpret_cast<unsigned long long*>(limbs + li);
-    if (d0) atomicAdd(L, static_cast<unsigned long long>(sg * d0));
-    if (d1) atomicAdd(L + 1, static_cast<unsigned long long>(sg * d1));
-    if (d2) atomicAdd(L + 2, static_cast<unsigned long long>(sg * static_cast<long long>(d2)));
+    long long* L = limbs + li;
+    if (d0) smem_add64(L, sg * d0);
+    if (d1) smem_add64(L + 1, sg * d1);
+    if (d2) smem_add64(L + 2, sg * static_cast<long long>(d2));
     LBK_XSTAT(0);
 }
 
