@@ -508,6 +508,63 @@ inline double nrm2(const DenseVector& x)
     return r;
 }
 
+// kernels.hpp:58-60, 99-113: the BabelStream-style calibration set and the
+// flops sweep (reference.cpp:92-130, fma_chain.hpp)
+enum class StreamOp { copy, mul, add, triad, dot };
+inline const char* to_string(StreamOp op)
+{
+    switch (op) {
+    case StreamOp::copy: return "copy";
+    case StreamOp::mul: return "mul";
+    case StreamOp::add: return "add";
+    case StreamOp::triad: return "triad";
+    case StreamOp::dot: return "dot";
+    }
+    return "?";
+}
+/// copy c<-a, mul b<-scalar*c, add c<-a+b, triad a<-b+scalar*c; returns the
+/// dot product for StreamOp::dot and 0 otherwise (kernels.hpp:99-103).
+inline double stream_kernel(StreamOp op, DenseVector& a, DenseVector& b, DenseVector& c,
+                            double scalar)
+{
+    detail::same_size(a.size(), b.size(), "stream_kernel");
+    detail::same_size(a.size(), c.size(), "stream_kernel");
+    auto e = a.executor();
+    const auto n = static_cast<int64_t>(a.size());
+    double r = 0.0;
+    lbk_status st = LBK_OK;
+    switch (op) {
+    case StreamOp::copy: st = lbk_stream_copy_f64(e->handle(), n, a.values.as<double>(), c.values.as<double>()); break;
+    case StreamOp::mul: st = lbk_stream_mul_f64(e->handle(), n, scalar, c.values.as<double>(), b.values.as<double>()); break;
+    case StreamOp::add:
+        st = lbk_stream_add_f64(e->handle(), n, a.values.as<double>(), b.values.as<double>(), c.values.as<double>());
+        break;
+    case StreamOp::triad:
+        st = lbk_stream_triad_f64(e->handle(), n, scalar, b.values.as<double>(), c.values.as<double>(),
+                                  a.values.as<double>());
+        break;
+    case StreamOp::dot: st = lbk_stream_dot_f64(e->handle(), n, a.values.as<double>(), b.values.as<double>(), &r); break;
+    }
+    detail::check(st, e->handle());
+    e->synchronize();
+    return r;
+}
+/// x_i <- fma_chain(x_i, fma_per_element) (kernels.hpp:105-109).
+inline void flops_sweep(DenseVector& x, int fma_per_element)
+{
+    if (fma_per_element < 0) throw UsageError("fma count must be nonnegative");
+    auto e = x.executor();
+    detail::check(lbk_flops_sweep_f64(e->handle(), static_cast<int64_t>(x.size()), fma_per_element,
+                                      x.values.as<double>()),
+                  e->handle());
+    e->synchronize();
+}
+/// Bytes touched by one stream op over n doubles (api.cpp:170-182).
+inline std::size_t stream_bytes(StreamOp op, std::size_t n)
+{
+    return (op == StreamOp::add || op == StreamOp::triad ? 3 : 2) * n * sizeof(double);
+}
+
 namespace detail {
 template <class M>
 void spmv_checks(const M& A, const DenseVector& x, const DenseVector& y, const char* what)

@@ -572,6 +572,50 @@ def nrm2(x: DenseVector) -> float:
     return out.value
 
 
+# ---------------------------------------------- stream set / flops sweep
+STREAM_OPS = ("copy", "mul", "add", "triad", "dot")
+
+
+def stream_bytes(op: str, n: int) -> int:
+    """Bytes touched by one stream op over n doubles (api.cpp:170-182)."""
+    return (3 if op in ("add", "triad") else 2) * n * 8
+
+
+def stream_kernel(op: str, a: DenseVector, b: DenseVector, c: DenseVector,
+                  scalar: float) -> float:
+    """kernels.hpp:99-103: copy c<-a, mul b<-scalar*c, add c<-a+b, triad
+    a<-b+scalar*c; returns the dot product for 'dot' and 0 otherwise."""
+    if op not in STREAM_OPS:
+        raise UsageError(f"unknown stream op '{op}'")
+    _same_size(a.size(), b.size(), "stream_kernel")
+    _same_size(a.size(), c.size(), "stream_kernel")
+    lib, ctx, n = L.load(), a.exec.ctx, a.size()
+    pa, pb, pc = _ptr(a.values), _ptr(b.values), _ptr(c.values)
+    out = C.c_double(0.0)
+    if op == "copy":
+        st = lib.lbk_stream_copy_f64(ctx, n, pa, pc)
+    elif op == "mul":
+        st = lib.lbk_stream_mul_f64(ctx, n, float(scalar), pc, pb)
+    elif op == "add":
+        st = lib.lbk_stream_add_f64(ctx, n, pa, pb, pc)
+    elif op == "triad":
+        st = lib.lbk_stream_triad_f64(ctx, n, float(scalar), pb, pc, pa)
+    else:
+        st = lib.lbk_stream_dot_f64(ctx, n, pa, pb, C.byref(out))
+    _check(st, ctx)
+    a.exec.synchronize()
+    return out.value
+
+
+def flops_sweep(x: DenseVector, fma_per_element: int) -> None:
+    """kernels.hpp:105-109: x_i <- fma_chain(x_i, fma_per_element)."""
+    if fma_per_element < 0:
+        raise UsageError("fma count must be nonnegative")
+    _check(L.load().lbk_flops_sweep_f64(x.exec.ctx, x.size(), int(fma_per_element), _ptr(x.values)),
+           x.exec.ctx)
+    x.exec.synchronize()
+
+
 # -------------------------------------------------------------------- SpMV
 _SPMV = {
     (CsrMatrix, torch.float64): ("lbk_spmv_csr_f64", "lbk_spmv_csr_adv_f64"),

@@ -328,3 +328,41 @@ def test_sellp_stream_kernel_opt_in():
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+# ------------------------------------------------ stream set / flops sweep
+def test_stream_ops_and_flops_sweep(O, ex, lk):
+    """The rest of the reference's StreamOp set and flops_sweep
+    (kernels.hpp:58-113, reference.cpp:92-130): closed-form values as the
+    harness verifies them (harness.cpp:166-195, 236-249), bit-exact."""
+    import math
+    n = 1 << 20
+    rng = np.random.default_rng(4)
+    ah, bh, ch = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    mk = lambda h: lk.vector_from(ex, h)  # noqa: E731
+    a, b, c = mk(ah), mk(bh), mk(ch)
+    assert lk.stream_kernel("copy", a, b, c, 0.4) == 0.0
+    assert np.array_equal(lk.vector_to_host(c), ah)
+    a, b, c = mk(ah), mk(bh), mk(ch)
+    lk.stream_kernel("mul", a, b, c, 0.4)
+    assert np.array_equal(lk.vector_to_host(b), 0.4 * ch)
+    a, b, c = mk(ah), mk(bh), mk(ch)
+    lk.stream_kernel("add", a, b, c, 0.4)
+    assert np.array_equal(lk.vector_to_host(c), ah + bh)
+    a, b, c = mk(ah), mk(bh), mk(ch)
+    lk.stream_kernel("triad", a, b, c, 0.4)
+    assert np.array_equal(lk.vector_to_host(a), bh + 0.4 * ch)
+    a, b, c = mk(ah), mk(bh), mk(ch)
+    assert lk.stream_kernel("dot", a, b, c, 0.4) == math.fsum((ah * bh).tolist())
+    assert lk.stream_bytes("add", n) == 24 * n and lk.stream_bytes("dot", n) == 16 * n
+    # flops sweep: the fma chain bit for bit (seeded_values(n, 7) as the harness)
+    x0 = O.seeded_values(4099, 7)
+    for fma in (0, 1, 2, 7, 64):
+        want = x0.copy()
+        for k in range(fma):
+            want = (2.0 if k % 2 == 0 else 0.5) * want + 3.0
+        x = lk.vector_from(ex, x0)
+        lk.flops_sweep(x, fma)
+        assert np.array_equal(lk.vector_to_host(x), want), fma
+    with pytest.raises(lk.UsageError):
+        lk.flops_sweep(lk.vector_from(ex, x0), -1)
