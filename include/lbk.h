@@ -308,6 +308,24 @@ lbk_status lbk_solve_coo(lbk_ctx, const lbk_coo* A, const double* b, double* x,
                          const lbk_solver_cfg* cfg, lbk_solve_result* result,
                          double* history, int32_t history_cap);
 
+/* gmres_restart_cycle (krylov.hpp:62-89, krylov.cpp:308-406, 551-565): one
+ * restarted-GMRES cycle of `restart` steps from the x passed in (updated in
+ * place), no in-cycle stopping test; a subdiagonal below 1e-14 ends the
+ * cycle early (happy breakdown).  rel_residual = ||b - A x|| / ||b|| after
+ * the cycle (||b|| = 1 when b = 0).  basis_out (DEVICE, may be NULL)
+ * receives the cycle's orthonormal basis, basis_count vectors of nrows
+ * (steps + 1, or steps after a happy breakdown); basis_cap = vectors it
+ * holds. */
+typedef struct lbk_gmres_cycle_result {
+    double rel_residual;
+    int32_t steps;
+    int32_t happy_breakdown;
+    int32_t basis_count;
+} lbk_gmres_cycle_result;
+lbk_status lbk_gmres_restart_cycle_csr(lbk_ctx, const lbk_csr* A, const double* b, double* x,
+                                       int32_t restart, double* basis_out, int32_t basis_cap,
+                                       lbk_gmres_cycle_result* result);
+
 /* ------------------------------------------------- distributed (new) */
 /* Row-partitioned CSR over P ranks (the reference has no
  * distributed matrix).  Partition: contiguous row blocks,

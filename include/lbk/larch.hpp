@@ -710,6 +710,45 @@ inline DenseVector apply_operator(const CooMatrix& A, const DenseVector& v)
     return y;
 }
 
+// krylov.hpp:62-89: one restarted-GMRES cycle
+struct GmresCycleResult {
+    double rel_residual = 0.0;
+    int steps = 0;
+    bool happy_breakdown = false;
+};
+inline GmresCycleResult gmres_restart_cycle(const CsrMatrix& A, const DenseVector& b, DenseVector& x,
+                                            int restart,
+                                            std::vector<DenseVector>* basis_out = nullptr)
+{
+    if (restart < 1) throw ConfigurationError("restart must be positive");
+    detail::same_size(static_cast<std::size_t>(A.nrows), b.size(), "gmres_restart_cycle");
+    detail::same_size(static_cast<std::size_t>(A.nrows), x.size(), "gmres_restart_cycle");
+    auto e = A.executor();
+    const auto n = static_cast<std::size_t>(A.nrows);
+    DenseVector basis;
+    if (basis_out) basis = make_vector(e, n * static_cast<std::size_t>(restart + 1));
+    const auto d = A.desc();
+    lbk_gmres_cycle_result r{};
+    detail::check(lbk_gmres_restart_cycle_csr(e->handle(), &d, b.values.as<double>(),
+                                              x.values.as<double>(), restart,
+                                              basis_out ? basis.values.as<double>() : nullptr,
+                                              basis_out ? restart + 1 : 0, &r),
+                  e->handle());
+    if (basis_out) {
+        basis_out->clear();
+        for (int i = 0; i < r.basis_count; ++i) {
+            DenseVector v = make_vector(e, n);
+            detail::check(lbk_memcpy_d2d(e->handle(), v.values.as<double>(),
+                                         basis.values.as<double>() + static_cast<std::size_t>(i) * n,
+                                         n * sizeof(double)),
+                          e->handle());
+            basis_out->push_back(std::move(v));
+        }
+        e->synchronize();
+    }
+    return GmresCycleResult{r.rel_residual, r.steps, r.happy_breakdown != 0};
+}
+
 }  // namespace lbk::larch
 
 #endif  // LBK_LARCH_HPP

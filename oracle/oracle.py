@@ -115,6 +115,9 @@ def ref():
             "ref_csr_to_coo": (C.c_int, [C.c_int, C.c_int, i64, i32p, i32p, f64p, i32p, i32p, f64p]),
             "ref_validate": (C.c_int, [C.c_int, C.c_int, C.c_int, i64, i32p, i32p, f64p]),
             "ref_read_mm": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64), C.c_void_p, C.c_void_p, C.c_void_p]),
+            "ref_gmres_cycle": (C.c_int, [C.c_int, C.c_int, C.c_int, i64, i32p, i32p, f64p, f64p,
+                                          f64p, C.c_int, C.POINTER(C.c_double), i32p, C.c_void_p,
+                                          C.c_int]),
             "ref_measure_peak_bandwidth": (C.c_int, [C.c_int, C.c_int, i64, C.c_int,
                                                      C.POINTER(C.c_double)]),
             "ref_solve": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i64, i32p, i32p, f64p, f64p, f64p, C.c_int, C.c_double, C.c_int, C.c_int, f64p, C.c_int, i32p, f64p, C.POINTER(i64)]),
@@ -424,3 +427,17 @@ def ref_peak_bandwidth(exec_kind: int = 1, workers: int = 1, bytes_: int = 1 << 
     out = C.c_double()
     _chk(ref().ref_measure_peak_bandwidth(exec_kind, workers, bytes_, reps, C.byref(out)))
     return out.value
+
+
+def ref_gmres_cycle(a: Csr, b: np.ndarray, x0=None, restart: int = 10) -> dict:
+    """The reference's gmres_restart_cycle (krylov.hpp:78-89) on CSR."""
+    n = a.nrows
+    x = np.zeros(n) if x0 is None else np.array(x0, np.float64)
+    rel = C.c_double()
+    oi = np.zeros(3, np.int32)
+    basis = np.zeros((restart + 1, n))
+    _chk(ref().ref_gmres_cycle(0, 1, n, a.nnz, a.row_ptr, a.cols, a.vals,
+                               np.ascontiguousarray(b, np.float64), x, restart, C.byref(rel), oi,
+                               basis.ctypes.data_as(C.c_void_p), restart + 1))
+    return {"rel_residual": rel.value, "steps": int(oi[0]), "happy": bool(oi[1]),
+            "basis": basis[: int(oi[2])].copy(), "x": x}

@@ -365,6 +365,33 @@ int ref_solve(int exec_kind, int workers, int fmt, int kind, int n,
     });
 }
 
+/// gmres_restart_cycle (krylov.hpp:78-89) on CSR: one cycle from x (updated
+/// in place); out_i = {steps, happy, basis size}; *rel = rel_residual;
+/// basis (n * cap, may be null) receives the basis vectors.
+int ref_gmres_cycle(int exec_kind, int workers, int n, std::int64_t nnz, const int* ptr,
+                    const int* cols, const double* vals, const double* b, double* x,
+                    int restart, double* rel, int* out_i, double* basis, int cap)
+{
+    return guarded([&] {
+        auto exec = make_exec(exec_kind, workers);
+        auto bv = larch::vector_from(exec, sp(b, n));
+        auto xv = larch::vector_from(exec, sp(static_cast<const double*>(x), n));
+        auto a = make_csr(exec, n, n, nnz, ptr, cols, vals);
+        std::vector<larch::DenseVector> V;
+        auto r = larch::gmres_restart_cycle(a, bv, xv, restart, &V);
+        auto xo = larch::vector_to_host(xv);
+        std::memcpy(x, xo.data(), xo.size() * sizeof(double));
+        *rel = r.rel_residual;
+        out_i[0] = r.steps;
+        out_i[1] = r.happy_breakdown ? 1 : 0;
+        out_i[2] = static_cast<int>(V.size());
+        for (int i = 0; basis && i < static_cast<int>(V.size()) && i < cap; ++i) {
+            auto h = larch::vector_to_host(V[static_cast<std::size_t>(i)]);
+            std::memcpy(basis + static_cast<std::size_t>(i) * n, h.data(), h.size() * sizeof(double));
+        }
+    });
+}
+
 /// The reference's own host bandwidth calibration: measure_peak_bandwidth
 /// (harness.cpp:125-141) -- stream copy of `bytes` per array on the given
 /// executor, median of `reps`; GB/s to *out.

@@ -72,6 +72,11 @@ class lbk_solver_cfg(C.Structure):
                 ("gmres_restart", C.c_int32)]
 
 
+class lbk_gmres_cycle_result(C.Structure):
+    _fields_ = [("rel_residual", C.c_double), ("steps", C.c_int32),
+                ("happy_breakdown", C.c_int32), ("basis_count", C.c_int32)]
+
+
 class lbk_solve_result(C.Structure):
     _fields_ = [("converged", C.c_int32), ("iterations", C.c_int32),
                 ("final_rel_residual", C.c_double), ("elapsed", C.c_double),
@@ -149,6 +154,8 @@ SIGNATURES = {
     "lbk_validate_coo": (st, [vp, P(lbk_coo)]),
     "lbk_solve_csr": (st, [vp, P(lbk_csr), vp, vp, P(lbk_solver_cfg), P(lbk_solve_result), vp, i32]),
     "lbk_solve_coo": (st, [vp, P(lbk_coo), vp, vp, P(lbk_solver_cfg), P(lbk_solve_result), vp, i32]),
+    "lbk_gmres_restart_cycle_csr": (st, [vp, P(lbk_csr), vp, vp, i32, vp, i32,
+                                         P(lbk_gmres_cycle_result)]),
     "lbk_part_range": (st, [i32, i32, i32, P(i32), P(i32)]),
     "lbk_dist_map_create": (st, [i32, i32, i32, i32, i32, vp, vp, P(vp)]),
     "lbk_dist_map_info": (st, [vp, P(lbk_dist_map_info_t)]),

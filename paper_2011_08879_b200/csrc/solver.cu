@@ -1058,6 +1058,35 @@ __global__ void gmres_backsub_kernel(SolverState* st)
     st->flops += static_cast<long long>(steps) * steps;
 }
 
+// gmres_restart_cycle only: the cycle's last basis vector v_steps =
+// w / hnext (krylov.cpp:369-370 pushes it; the solver's own cycle skips it,
+// nothing reads it).  Not after a happy breakdown.
+struct OpGmLast {
+    static constexpr int NV = 1;
+    double* __restrict__ V;
+    long long ld;
+    const double* __restrict__ w;
+    SolverState* st;
+    double inv;
+    double* vout;
+    __device__ bool skip() const
+    {
+        return *(volatile int*)&st->done != 0 || *(volatile int*)&st->gm->happy != 0;
+    }
+    __device__ void prologue()
+    {
+        inv = 1.0 / st->gm->hnext;
+        vout = V + st->gm->steps * ld;
+    }
+    struct In {
+        double w;
+    };
+    __device__ In load(long long k) const { return {w[k]}; }
+    __device__ void elem(long long k, const In& in, auto*) const { vout[k] = mul_rn(in.w, inv); }
+    static constexpr bool kNoFinish = true;
+    __device__ void finish(const double*) const {}
+};
+
 // x += y_0 v_0 + y_1 v_1 + ... in the reference's axpy order (krylov.cpp:392-394)
 struct OpGmUpdate {
     static constexpr int NV = 1;
@@ -1619,9 +1648,19 @@ void finish_solve(lbk_ctx ctx, Env& env, SolverState* st, double* hist, double* 
     }
 }
 
+// gmres_restart_cycle (krylov.hpp:78-89): one cycle, its outcome, and
+// optionally the cycle's orthonormal basis (device, n per vector)
+struct CycleOut {
+    int steps = 0, happy = 0;
+    double rel = 0.0;
+    double* basis = nullptr;
+    int basis_cap = 0;
+    int basis_count = 0;
+};
+
 template <class Env>
 void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lbk_solver_cfg* cfg,
-                lbk_solve_result* res, double* history, int hist_cap)
+                lbk_solve_result* res, double* history, int hist_cap, CycleOut* cyc = nullptr)
 {
     NvtxRange nvtx_("lbk_solve");
     // krylov.cpp:449-472 validation
@@ -1655,7 +1694,9 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
     auto* st = bufs.get<SolverState>(1);
     auto* hist = bufs.get<double>(size_t(limit) + 2);
     // norm_b (krylov.cpp:478) -- host value needed for the zero-b rule
-    const double norm_b = env.norm(b);
+    double norm_b = env.norm(b);
+    // cycle_entry (krylov.cpp:551-565): a zero b normalises by 1
+    if (cyc && norm_b == 0.0) norm_b = 1.0;
     SolverState h{};
     h.limit = limit;
     h.fixed = fixed ? 1 : 0;
@@ -1721,6 +1762,46 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
             gmres_backsub_kernel<<<1, 1, 0, ctx->stream>>>(st);
             LBK_LAUNCH_CHECK();
             env.vec(OpGmUpdate{x, V, ne, st, 0});
+            if (cyc) {
+                // the cycle's steps and happy flag (before the residual kernel
+                // resets them for a next cycle), then its true residual into
+                // w (V keeps the basis)
+                GmresState gc{};
+                SolverState sc{};
+                LBK_CUDA(cudaMemcpyAsync(&gc, G, sizeof(gc), cudaMemcpyDeviceToHost, ctx->stream));
+                if (cyc->basis) env.vec(OpGmLast{V, ne, w, st, 0.0, nullptr});
+                env.apply(x, EpiGmRes{b, w, st, 0});
+                LBK_CUDA(cudaMemcpyAsync(&sc, st, sizeof(sc), cudaMemcpyDeviceToHost, ctx->stream));
+                env.sync();
+                need(sc.status != ST_BREAKDOWN, LBK_BREAKDOWN,
+                     std::string(breakdown_what(sc.breakdown_what)) + " at iteration " +
+                         std::to_string(sc.breakdown_iter));
+                cyc->steps = gc.steps;
+                cyc->happy = gc.happy;
+                cyc->rel = sc.last_rel;
+                int count = gc.happy ? gc.steps : gc.steps + 1;
+                if (gc.steps == 0) {  // b - A x == 0: happy, empty basis (krylov.cpp:317-324)
+                    cyc->happy = 1;
+                    cyc->rel = 0.0;
+                    count = 0;
+                }
+                cyc->basis_count = count;
+                if (cyc->basis) {
+                    need(count <= cyc->basis_cap, LBK_USAGE_ERROR,
+                         "gmres_restart_cycle: basis_out holds fewer than steps + 1 vectors");
+                    for (int i = 0; i < count && n; ++i)
+                        LBK_CUDA(cudaMemcpyAsync(cyc->basis + size_t(i) * n, V + size_t(i) * ne,
+                                                 size_t(n) * sizeof(double),
+                                                 cudaMemcpyDeviceToDevice, ctx->stream));
+                }
+                if (env.ext_x() && n)
+                    LBK_CUDA(cudaMemcpyAsync(x_user, x, size_t(n) * sizeof(double),
+                                             cudaMemcpyDeviceToDevice, ctx->stream));
+                env.sync();
+                cudaEventDestroy(ev0);
+                cudaEventDestroy(ev1);
+                return;
+            }
             env.apply(x, EpiGmRes{b, V, st, 0});
             env.vec(OpGmScale{V, nullptr, st, 0, 0.0});
             LBK_CUDA(cudaMemcpyAsync(done_host, &st->done, sizeof(int), cudaMemcpyDeviceToHost,
@@ -1874,6 +1955,46 @@ lbk_status lbk_solve_csr(lbk_ctx ctx, const lbk_csr* A, const double* b, double*
         }
         LocalEnv<CsrOp> env{ctx, op, red_ws(ctx, kRedMaxBlocks, 2), A->nrows, A->nnz};
         solve_impl(ctx, env, b, x, cfg, result, history, history_cap);
+    });
+}
+
+lbk_status lbk_gmres_restart_cycle_csr(lbk_ctx ctx, const lbk_csr* A, const double* b, double* x,
+                                       int32_t restart, double* basis_out, int32_t basis_cap,
+                                       lbk_gmres_cycle_result* result)
+{
+    if (!ctx || !A || !result) return LBK_USAGE_ERROR;
+    return guard(ctx, [&] {
+        need(restart >= 1, LBK_CONFIGURATION_ERROR, "restart must be positive");
+        need(A->dtype == LBK_F64, LBK_TYPE_ERROR, "gmres_restart_cycle: FP64 matrices only");
+        need(A->nrows == A->ncols, LBK_SHAPE_ERROR,
+             "solve requires a square matrix, got " + std::to_string(A->nrows) + "x" +
+                 std::to_string(A->ncols));
+        CsrOp op{CsrView<double>{A->nrows, A->ncols, A->nnz, A->row_ptr, A->col_idx,
+                                 static_cast<const double*>(A->vals), A->tile_rows, A->ntiles}};
+        if (!op.A.tile_rows && A->nrows > 0 && aligned16(A->vals) && aligned16(A->col_idx)) {
+            op.A.ntiles = csr_ntiles(A->nnz, A->nrows);
+            int* plan = static_cast<int*>(scratch(ctx, size_t(op.A.ntiles + 1) * sizeof(int)));
+            csr_plan_launch(ctx, A->row_ptr, A->nrows, A->nnz, plan);
+            op.A.tile_rows = plan;
+        }
+        LocalEnv<CsrOp> env{ctx, op, red_ws(ctx, kRedMaxBlocks, 2), A->nrows, A->nnz};
+        // one cycle of `restart` steps, no in-cycle stop (cycle_entry,
+        // krylov.cpp:551-565: CycleControl tol = -1)
+        lbk_solver_cfg cfg{};
+        cfg.kind = 3;
+        cfg.max_iters = restart;
+        cfg.rel_tol = 1.0;
+        cfg.fixed_iters = restart;
+        cfg.gmres_restart = restart;
+        lbk_solve_result res{};
+        CycleOut cyc;
+        cyc.basis = basis_out;
+        cyc.basis_cap = basis_cap;
+        solve_impl(ctx, env, b, x, &cfg, &res, nullptr, 0, &cyc);
+        result->rel_residual = cyc.rel;
+        result->steps = cyc.steps;
+        result->happy_breakdown = cyc.happy;
+        result->basis_count = cyc.basis_count;
     });
 }
 

@@ -710,6 +710,41 @@ class SolveResult:
     flop_count: int = 0
 
 
+@dataclass
+class GmresCycleResult:
+    """krylov.hpp:62-66."""
+    rel_residual: float
+    steps: int
+    happy_breakdown: bool
+
+
+def gmres_restart_cycle(matrix: "CsrMatrix", b: DenseVector, x: DenseVector, restart: int,
+                        basis_out: Optional[list] = None) -> GmresCycleResult:
+    """krylov.hpp:68-89: one restarted-GMRES cycle (modified Gram-Schmidt
+    basis of dimension <= restart, Givens least squares, x updated); a
+    subdiagonal below 1e-14 ends it early with the happy flag.  basis_out,
+    when given, receives the cycle's orthonormal basis vectors."""
+    if not isinstance(matrix, CsrMatrix):
+        raise DispatchError("gmres_restart_cycle: CSR matrices only")
+    if restart < 1:
+        raise ConfigurationError("restart must be positive")
+    _same_size(matrix.nrows, b.size(), "gmres_restart_cycle")
+    _same_size(matrix.nrows, x.size(), "gmres_restart_cycle")
+    ex = matrix.exec
+    basis = ex.empty((restart + 1) * matrix.nrows, torch.float64) if basis_out is not None else None
+    d = matrix.desc()
+    r = L.lbk_gmres_cycle_result()
+    _check(L.load().lbk_gmres_restart_cycle_csr(ex.ctx, C.byref(d), _ptr(b.values), _ptr(x.values),
+                                                int(restart), _ptr(basis),
+                                                restart + 1 if basis is not None else 0,
+                                                C.byref(r)), ex.ctx)
+    if basis_out is not None:
+        basis_out.clear()
+        for i in range(r.basis_count):
+            basis_out.append(DenseVector(basis[i * matrix.nrows:(i + 1) * matrix.nrows].clone(), ex))
+    return GmresCycleResult(r.rel_residual, r.steps, bool(r.happy_breakdown))
+
+
 def solve(matrix, b: DenseVector, x: DenseVector, config: SolverConfig) -> SolveResult:
     """krylov.hpp:53-56 solve(A, b, x, cfg): x in/out, device-resident."""
     if isinstance(matrix, (CsrMatrix, CooMatrix)) and matrix.nrows != matrix.ncols:

@@ -363,3 +363,45 @@ def test_cfg5_report_vs_reference():
     assert first(h, 1e-6) == first(hr, 1e-6) == 275
     assert np.max(np.abs(h[:40] - hr[:40]) / hr[:40]) <= 1e-6
     assert r.final_rel_residual <= 1e-8
+
+
+# ------------------------------------------------------ gmres_restart_cycle
+@pytest.mark.parametrize("m,restart", [(12, 10), (10, 40)])
+def test_gmres_restart_cycle_vs_reference(R, lk, ex, m, restart):
+    """gmres_restart_cycle (krylov.hpp:78-89) against the reference
+    library's: the same step count and happy flag, the residual and x to
+    rounding, an orthonormal basis matching the reference's to rounding."""
+    O = R
+    A = O.stencil("7pt", m, 0.5)
+    b = O.spmv_csr(A, O.seeded_values(A.nrows, 11))
+    ref = O.ref_gmres_cycle(A, b, restart=restart)
+    Ad = lk.csr_from_host(ex, A.nrows, A.ncols, A.row_ptr, A.cols, A.vals)
+    x = lk.zeros(ex, A.nrows)
+    basis = []
+    r = lk.gmres_restart_cycle(Ad, lk.vector_from(ex, b), x, restart, basis)
+    assert r.steps == ref["steps"] and r.happy_breakdown == ref["happy"]
+    assert abs(r.rel_residual - ref["rel_residual"]) <= 1e-6 * ref["rel_residual"] + 1e-15
+    assert np.max(np.abs(lk.vector_to_host(x) - ref["x"])) <= 1e-9 * np.max(np.abs(ref["x"]))
+    assert len(basis) == len(ref["basis"])
+    V = np.stack([lk.vector_to_host(v) for v in basis])
+    # the leading Krylov vectors to rounding; later ones amplify the dot
+    # rounding differences as the residual falls (ill-conditioned
+    # directions), so they are held to the orthonormality both bases share
+    k = min(6, len(basis))
+    assert np.max(np.abs(V[:k] - ref["basis"][:k])) <= 1e-8
+    G = V[:k] @ V[:k].T
+    assert np.max(np.abs(G - np.eye(k))) <= 1e-10
+    assert np.allclose(np.linalg.norm(V, axis=1), 1.0, atol=1e-12)
+
+
+def test_gmres_restart_cycle_edge_cases(lk, ex, O):
+    A = O.stencil("7pt", 6)
+    Ad = lk.csr_from_host(ex, A.nrows, A.ncols, A.row_ptr, A.cols, A.vals)
+    # x already exact: zero residual -> happy, no steps, empty basis
+    b = O.spmv_csr(A, np.ones(A.nrows))
+    basis = []
+    r = lk.gmres_restart_cycle(Ad, lk.vector_from(ex, b), lk.vector_from(ex, np.ones(A.nrows)), 5,
+                               basis)
+    assert r.steps == 0 and r.happy_breakdown and r.rel_residual == 0.0 and basis == []
+    with pytest.raises(lk.ConfigurationError):
+        lk.gmres_restart_cycle(Ad, lk.vector_from(ex, b), lk.zeros(ex, A.nrows), 0)
