@@ -133,6 +133,9 @@ __global__ void coo_plan_kernel(const int* __restrict__ rows, long long nnz, int
 //     (warp_row_global), the rest of that tile is staged.
 // The tile size is chosen per matrix (one warp pass of 32*G rows of mean
 // length): see stream_tile_nnz().
+#ifndef LBK_CSR_MINB
+#define LBK_CSR_MINB 2  // CTAs per SM the CSR stream kernel is register-budgeted for
+#endif
 #ifndef LBK_CSR_CAP
 #define LBK_CSR_CAP 1024
 #endif
@@ -349,7 +352,11 @@ __device__ __forceinline__ void staged_rows(int rb, int re, T* sv, const int* sc
                 hi = hi > e.x + e.y ? hi : e.x + e.y;
             }
         }
+#ifdef LBK_NO_FASTPATH
+        if (false) {
+#else
         if (!__any_sync(0xffffffffu, any_long)) {
+#endif
             T v[G][CH], g[G][CH];
 #pragma unroll
             for (int q = 0; q < G; ++q) {
@@ -590,7 +597,7 @@ __device__ __forceinline__ void warp_tile_loop(int ntiles, long long nnz, const 
 }
 
 template <typename T, class Epi, int G>
-__global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), 2)
+__global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), LBK_CSR_MINB)
     csr_stream_kernel(CsrView<T> A, const T* __restrict__ x, Epi epi, RedWs ws)
 {
     pdl_enter();
