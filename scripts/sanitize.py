@@ -29,6 +29,22 @@ for kind in ("cg", "bicgstab", "cgs", "gmres"):
     xs = lk.zeros(ex, A7.nrows)
     lk.solve(A7, b, xs, lk.SolverConfig(kind=kind, rel_tol=1e-8, max_iters=200, gmres_restart=10))
 lk.dot(x, x)
+# exact reductions: the direct-to-limbs path (600 decades of range),
+# cancellation, subnormals, inf/nan (xred.cuh)
+rng = np.random.default_rng(1)
+w = rng.standard_normal(200000) * 10.0 ** rng.integers(-300, 300, 200000)
+lk.dot(lk.vector_from(ex, w), lk.vector_from(ex, np.ones(w.size)))
+w[5] = np.inf
+w[7] = np.nan
+lk.dot(lk.vector_from(ex, w), lk.vector_from(ex, np.ones(w.size)))
+v = rng.standard_normal(4096) * 1e-160
+lk.dot(lk.vector_from(ex, v), lk.vector_from(ex, v))
+# calibration set, flops sweep, one GMRES cycle with its basis
+sa, sb, sc = (lk.vector_from(ex, rng.standard_normal(1 << 16)) for _ in range(3))
+for op in lk.STREAM_OPS:
+    lk.stream_kernel(op, sa, sb, sc, 0.4)
+lk.flops_sweep(sa, 9)
+lk.gmres_restart_cycle(A7, b, lk.zeros(ex, A7.nrows), 8, [])
 M = lk.coo_from_entries(ex, 5, 5, [(0, 1, 1.0), (4, 4, 2.0), (0, 1, 3.0)])
 lk.coo_to_csr(M)
 torch.cuda.synchronize()
