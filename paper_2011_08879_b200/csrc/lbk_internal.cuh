@@ -373,12 +373,14 @@ __device__ __forceinline__ bool grid_reduce(RAcc (&acc)[NV], RedWs ws, int tid, 
             G[i] = 0;
         }
         __syncthreads();
-        if (tid == 0) {
+        if (tid < 32) {  // warp 0 rounds (xred_round_warp), thread 0 finishes
             double tot[NV];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) tot[v] = xred_round(g_xsh + v * kXV);
-            fin(tot);
-            *ws.counter = 0;
+            for (int v = 0; v < NV; ++v) tot[v] = xred_round_warp(g_xsh + v * kXV);
+            if (tid == 0) {
+                fin(tot);
+                *ws.counter = 0;
+            }
         }
         return true;
     }

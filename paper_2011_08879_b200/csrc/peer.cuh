@@ -219,80 +219,148 @@ __device__ __forceinline__ double peer_allreduce_warp(const PeerDev& pd, double 
 
 // Exact variant (xred.cuh).  One warp.  L (shared memory) holds nv values
 // of raw limbs (kXV int64 each) -- this rank's exact totals; on return it
-// holds the exact sum over all ranks (raw limbs, round with xred_round).
+// holds the exact sum over all ranks (raw limbs, round with xred_round_warp).
 // Each rank posts every value as a header {lo:8 | cnt:8 | neg:1 | pinf:1 |
-// ninf:1 | nan:1} and cnt sign-magnitude digits; integer sums make the
-// result independent of rank order and of the partition.
+// ninf:1 | nan:1 | raw:1} and either cnt raw limbs (two words each) or cnt
+// sign-magnitude digits; integer sums make the result independent of rank
+// order and of the partition.
 __device__ __forceinline__ void peer_xallreduce_warp(const PeerDev& pd, long long* L, int nv)
 {
     const int lane = threadIdx.x & 31;
     PeerHdr* me = pd.win[pd.rank];
-    __shared__ unsigned hdr[kXMaxNV];
-    if (lane == 0) {
-        for (int v = 0; v < nv; ++v) {
-            long long* X = L + v * kXV;
-            long long c = 0;
-            for (int i = 0; i < kXL; ++i) {
-                const long long t = X[i] + c;
-                c = t >> 32;
-                X[i] = t & 0xffffffffLL;
+    // this rank's values.  Normally the raw limbs' nonzero range, two words
+    // per limb {lo32, hi32} (no normalisation pass); a value whose range
+    // does not fit its 80-word box (> 39 limbs, only for data spanning
+    // ~1250 bits) goes as normalised sign-magnitude digits instead
+    unsigned hdr[kXMaxNV];
+    int lo_l[kXMaxNV];
+    XMag mg[kXMaxNV];
+#pragma unroll
+    for (int v = 0; v < kXMaxNV; ++v) {
+        if (v >= nv) break;
+        const long long* X = L + v * kXV;
+        int l0 = 99, h0 = -1;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int i = lane + 32 * k;
+            if (i < kXL && X[i] != 0) {
+                l0 = l0 < i ? l0 : i;
+                h0 = i;
             }
-            const bool neg = c < 0;
-            if (neg) {
-                long long cy = 1;
-                for (int i = 0; i < kXL; ++i) {
-                    const long long t = (0xffffffffLL - X[i]) + cy;
-                    cy = t >> 32;
-                    X[i] = t & 0xffffffffLL;
+        }
+        l0 = __reduce_min_sync(0xffffffffu, l0);
+        h0 = __reduce_max_sync(0xffffffffu, h0);
+        const int cnt = h0 < 0 ? 0 : h0 - l0 + 1;
+        const unsigned fl = (X[kXPinf] ? 1u << 17 : 0u) | (X[kXNinf] ? 1u << 18 : 0u) |
+                            (X[kXNan] ? 1u << 19 : 0u);
+        if (2 * cnt + 1 <= kXV) {
+            lo_l[v] = h0 < 0 ? 0 : l0;
+            hdr[v] = static_cast<unsigned>(lo_l[v]) | (static_cast<unsigned>(cnt) << 8) | fl |
+                     (1u << 20);
+        } else {
+            mg[v] = xred_mag_warp(X);
+            int kl = 3, kh = -1;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                if (mg[v].d[k]) {
+                    kl = kl < k ? kl : k;
+                    kh = k;
                 }
+            const unsigned m = __ballot_sync(0xffffffffu, kh >= 0);
+            int lo = 0, dc = 0;
+            if (m) {
+                const int ll = __ffs(m) - 1, hl = 31 - __clz(static_cast<int>(m));
+                lo = 3 * ll + __shfl_sync(0xffffffffu, kl, ll);
+                dc = 3 * hl + __shfl_sync(0xffffffffu, kh, hl) - lo + 1;
             }
-            int lo = 0, hi = -1;
-            for (int i = 0; i < kXL; ++i)
-                if (X[i]) {
-                    if (hi < 0) lo = i;
-                    hi = i;
-                }
-            const int cnt = hi < 0 ? 0 : hi - lo + 1;
-            hdr[v] = static_cast<unsigned>(lo) | (static_cast<unsigned>(cnt) << 8) |
-                     (neg ? 1u << 16 : 0u) | (X[kXPinf] ? 1u << 17 : 0u) |
-                     (X[kXNinf] ? 1u << 18 : 0u) | (X[kXNan] ? 1u << 19 : 0u);
+            lo_l[v] = lo;
+            hdr[v] = static_cast<unsigned>(lo) | (static_cast<unsigned>(dc) << 8) |
+                     (mg[v].neg ? 1u << 16 : 0u) | fl;
         }
     }
-    __syncwarp();
     const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&me->seq_r) + 1;
     const int par = static_cast<int>(e & 1);
     const unsigned e32 = static_cast<unsigned>(e);
     const unsigned long long tag = static_cast<unsigned long long>(e32) << 32;
-    for (int v = 0; v < nv; ++v) {
+#pragma unroll
+    for (int v = 0; v < kXMaxNV; ++v) {
+        if (v >= nv) break;
         const unsigned h = hdr[v];
-        const int lo = h & 0xff, cnt = (h >> 8) & 0xff;
-        for (int w = lane; w <= cnt; w += 32) {
-            const unsigned pay = w == 0 ? h : static_cast<unsigned>(L[v * kXV + lo + w - 1]);
-            for (int q = 0; q < pd.P; ++q)
-                st_volatile_u64(&pd.win[q]->xred_ll[par][pd.rank][v * kXV + w], tag | pay);
+        const bool raw = (h >> 20) & 1;
+        const int cnt = (h >> 8) & 0xff;
+        const int nw = raw ? 2 * cnt : cnt;
+        for (int w0 = 0; w0 <= nw; w0 += 32) {  // whole-warp rounds: shuffles inside
+            const int w = w0 + lane;
+            unsigned pay = h;
+            if (raw) {
+                if (w > 0 && w <= nw) {
+                    const long long lv = L[v * kXV + lo_l[v] + (w - 1) / 2];
+                    pay = (w & 1) ? static_cast<unsigned>(lv)
+                                  : static_cast<unsigned>(static_cast<unsigned long long>(lv) >> 32);
+                }
+            } else {
+                const unsigned dg = xred_digit(mg[v], lo_l[v] + w - 1);
+                if (w > 0) pay = dg;
+            }
+            if (w <= nw)
+                for (int q = 0; q < pd.P; ++q)
+                    st_volatile_u64(&pd.win[q]->xred_ll[par][pd.rank][v * kXV + w], tag | pay);
         }
     }
     __syncwarp();
     for (int i = lane; i < nv * kXV; i += 32) L[i] = 0;
     __syncwarp();
-    for (int q = 0; q < pd.P; ++q) {
-        for (int v = 0; v < nv; ++v) {
-            const unsigned long long* box = me->xred_ll[par][q] + v * kXV;
-            const unsigned h = peer_ll_read32(box, e32, me, 2, q, e);
-            const int lo = h & 0xff, cnt = (h >> 8) & 0xff;
-            const bool neg = (h >> 16) & 1;
-            for (int w = lane; w < cnt; w += 32) {
-                const long long d = peer_ll_read32(box + 1 + w, e32, me, 2, q, e);
-                L[v * kXV + lo + w] += neg ? -d : d;
+    // receive in parallel (not rank after rank): one round of header loads
+    // (lane = (rank, value), P * nv <= 32), then every posted digit of every
+    // rank as one flat item list, 32 loads in flight per round; the digits
+    // are added into the limbs with shared atomics (order-free)
+    const int nh = pd.P * nv;
+    unsigned hh = 0;
+    int hq = 0, hv = 0;
+    if (lane < nh) {
+        hq = lane / nv;
+        hv = lane % nv;
+        hh = peer_ll_read32(me->xred_ll[par][hq] + hv * kXV, e32, me, 2, hq, e);
+        if (hh & (1u << 17)) smem_add64(L + hv * kXV + kXPinf, 1);
+        if (hh & (1u << 18)) smem_add64(L + hv * kXV + kXNinf, 1);
+        if (hh & (1u << 19)) smem_add64(L + hv * kXV + kXNan, 1);
+    }
+    const int hcnt = lane < nh ? static_cast<int>((hh >> 8) & 0xff) : 0;
+    int incl = hcnt;  // inclusive prefix of the digit counts over header lanes
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int i0 = 0; i0 < total; i0 += 32) {
+        const int it = i0 + lane;
+        // owner header lane: the first with incl > it
+        int o = 0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const int t = __shfl_sync(0xffffffffu, incl, o + d - 1);
+            if (o + d - 1 < 32 && t <= it) o += d;
+        }
+        const int start = __shfl_sync(0xffffffffu, incl - hcnt, o);
+        const unsigned oh = __shfl_sync(0xffffffffu, hh, o);
+        const int oq = __shfl_sync(0xffffffffu, hq, o), ov = __shfl_sync(0xffffffffu, hv, o);
+        if (it < total) {
+            const int w = it - start;
+            const unsigned long long* box = me->xred_ll[par][oq] + ov * kXV;
+            long long d;
+            if ((oh >> 20) & 1) {  // a raw limb: {lo32, hi32}
+                const unsigned lo32 = peer_ll_read32(box + 1 + 2 * w, e32, me, 2, oq, e);
+                const unsigned hi32 = peer_ll_read32(box + 2 + 2 * w, e32, me, 2, oq, e);
+                d = static_cast<long long>((static_cast<unsigned long long>(hi32) << 32) | lo32);
+            } else {
+                d = peer_ll_read32(box + 1 + w, e32, me, 2, oq, e);
+                if ((oh >> 16) & 1) d = -d;
             }
-            if (lane == 0) {
-                L[v * kXV + kXPinf] += (h >> 17) & 1;
-                L[v * kXV + kXNinf] += (h >> 18) & 1;
-                L[v * kXV + kXNan] += (h >> 19) & 1;
-            }
-            __syncwarp();
+            smem_add64(L + ov * kXV + (oh & 0xff) + w, d);
         }
     }
+    __syncwarp();
     if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(&me->seq_r) = e;
     __syncwarp();
 }

@@ -1319,23 +1319,39 @@ __global__ void peer_flush_cg_kernel(E3 e3, const double* base, int has_a, int h
 // no combine step); the slot is summed over ranks (NCCL int64 allreduce /
 // host sums / peer digit posts) and rounded once, so every rank and every
 // rank count sees the same bits as the single-GPU solver.
+// Move a deferred slot (n int64, n <= 5 * 32) into shared memory and zero
+// it: all loads first (one round trip), then the stores.  One warp.
+__device__ __forceinline__ void take_slot(long long* L, long long* slot, int n)
+{
+    const int lane = threadIdx.x & 31;
+    long long v[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = lane + 32 * k;
+        v[k] = i < n ? __ldcg(slot + i) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = lane + 32 * k;
+        if (i < n) {
+            L[i] = v[k];
+            slot[i] = 0;
+        }
+    }
+}
+
 template <class E>
 __global__ void xfinish_kernel(E e, long long* slot)
 {
     constexpr int NV = E::NV > 0 ? E::NV : 1;
     __shared__ long long L[NV * kXV];
     if (e.skip()) return;
-    for (int i = threadIdx.x; i < NV * kXV; i += blockDim.x) {
-        L[i] = slot[i];
-        slot[i] = 0;
-    }
+    take_slot(L, slot, NV * kXV);
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double t[NV];
+    double t[NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) t[v] = xred_round(L + v * kXV);
-        e.finish(t);
-    }
+    for (int v = 0; v < NV; ++v) t[v] = xred_round_warp(L + v * kXV);
+    if (threadIdx.x == 0) e.finish(t);
 }
 
 template <class E>
@@ -1346,18 +1362,13 @@ __global__ void peer_xfinish_kernel(E e, long long* slot, PeerDev pd)
     __shared__ long long L[NV * kXV];
     if (e.skip()) return;
     const int lane = threadIdx.x;
-    for (int i = lane; i < NV * kXV; i += 32) {
-        L[i] = slot[i];
-        slot[i] = 0;
-    }
+    take_slot(L, slot, NV * kXV);
     __syncwarp();
     peer_xallreduce_warp(pd, L, NV);
-    if (lane == 0) {
-        double t[NV];
+    double t[NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) t[v] = xred_round(L + v * kXV);
-        e.finish(t);
-    }
+    for (int v = 0; v < NV; ++v) t[v] = xred_round_warp(L + v * kXV);
+    if (lane == 0) e.finish(t);
 }
 
 // exact-mode twin of peer_finish_cg_kernel: K1's <p,Ap> (slot s1) and the
@@ -1370,12 +1381,10 @@ __global__ void peer_xfinish_cg_kernel(E1 e1, E3 e3, long long* s1, long long* s
     if (e1.skip()) return;
     const int lane = threadIdx.x;
     const bool pending = e1.st->res_pending != 0;
-    for (int i = lane; i < kXV; i += 32) {
-        L[i] = s1[i];
-        s1[i] = 0;
-        L[kXV + i] = pending ? s3[i] : 0;
-        if (pending) s3[i] = 0;
-    }
+    take_slot(L, s1, kXV);
+    if (pending) take_slot(L + kXV, s3, kXV);
+    else
+        for (int i = lane; i < kXV; i += 32) L[kXV + i] = 0;
     __syncwarp();
     // the pending residual goes first so its finish runs before K1's
     if (pending) {
@@ -1387,13 +1396,13 @@ __global__ void peer_xfinish_cg_kernel(E1 e1, E3 e3, long long* s1, long long* s
         __syncwarp();
     }
     peer_xallreduce_warp(pd, L, pending ? 2 : 1);
+    const double t3 = pending ? xred_round_warp(L) : 0.0;
+    const double t1 = xred_round_warp(pending ? L + kXV : L);
     if (lane == 0) {
         if (pending) {
-            const double t3 = xred_round(L);
             e3.finish(&t3);
             if (e1.st->done) return;
         }
-        const double t1 = xred_round(pending ? L + kXV : L);
         e1.finish(&t1);
         e1.st->res_pending = 1;
     }
@@ -1406,16 +1415,11 @@ __global__ void peer_xflush_cg_kernel(E3 e3, long long* s3, PeerDev pd)
     __shared__ long long L[kXV];
     if (e3.skip() || !e3.st->res_pending) return;
     const int lane = threadIdx.x;
-    for (int i = lane; i < kXV; i += 32) {
-        L[i] = s3[i];
-        s3[i] = 0;
-    }
+    take_slot(L, s3, kXV);
     __syncwarp();
     peer_xallreduce_warp(pd, L, 1);
-    if (lane == 0) {
-        const double t = xred_round(L);
-        e3.finish(&t);
-    }
+    const double t = xred_round_warp(L);
+    if (lane == 0) e3.finish(&t);
 }
 
 // ||b|| of the distributed right-hand side (exact mode)

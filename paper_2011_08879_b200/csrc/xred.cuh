@@ -255,51 +255,142 @@ __device__ __forceinline__ void xred_begin()
     __syncthreads();
 }
 
-// Round a value's limbs to the nearest double (ties to even), in place
-// (L is scratch afterwards).  Single thread.
-static __device__ __noinline__ double xred_round(long long* L)
+// ------------------------------------------------- warp-parallel finish
+// The finishing steps run on one warp, not one thread: lane j owns digits
+// 3j .. 3j+2 (72 digits), the carries ripple between lanes with shuffles
+// (a carry survives a digit only when it is all ones or zero, so the loop
+// ends after one or two rounds), and sign, top digit and sticky bits come
+// from ballots.  This is the fixed cost of every reduction (the last
+// block on one GPU, the finish kernel per exchange in the distributed
+// solver), so it matters most at 8 ranks.
+struct XMag {
+    unsigned d[3];  // magnitude digits 3*lane .. 3*lane+2
+    bool neg;
+    int special;    // 0 finite, 1 +inf, 2 -inf, 3 nan
+};
+
+// All 32 lanes call.  L: one value's raw limbs (kXV int64, read only).
+__device__ __forceinline__ XMag xred_mag_warp(const long long* L)
 {
-    if (L[kXNan] || (L[kXPinf] && L[kXNinf])) return __longlong_as_double(0x7ff8000000000000LL);
-    if (L[kXPinf]) return __longlong_as_double(0x7ff0000000000000LL);
-    if (L[kXNinf]) return __longlong_as_double(static_cast<long long>(0xfff0000000000000ULL));
-    // normalise to digits in [0, 2^32); the final carry is the sign (0 / -1)
-    long long c = 0;
-    for (int i = 0; i < kXL; ++i) {
-        const long long t = L[i] + c;
-        c = t >> 32;  // floor
-        L[i] = t & 0xffffffffLL;
+    const int lane = threadIdx.x & 31;
+    XMag r;
+    const long long pinf = L[kXPinf], ninf = L[kXNinf], nan = L[kXNan];
+    r.special = (nan || (pinf && ninf)) ? 3 : (pinf ? 1 : (ninf ? 2 : 0));
+    long long t[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int i = 3 * lane + k;
+        t[k] = i < kXL - 1 ? L[i] : 0;
     }
-    const bool neg = c < 0;
-    if (neg) {  // magnitude = ~D + 1 over the digits
-        long long cy = 1;
-        for (int i = 0; i < kXL; ++i) {
-            const long long v = (0xffffffffLL - L[i]) + cy;
-            cy = v >> 32;
-            L[i] = v & 0xffffffffLL;
+    long long sign = L[kXL - 1];  // limb 72
+    long long c = 0;              // this lane's carry out
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const long long v = t[k] + c;
+        c = v >> 32;
+        t[k] = v & 0xffffffffLL;
+    }
+    // ripple the carries up the lanes (lane 23's carry goes to the sign)
+    for (;;) {
+        if (lane == 23) {
+            sign += c;
+            c = 0;
+        }
+        const long long cin = __shfl_up_sync(0xffffffffu, c, 1);
+        const bool more = __any_sync(0xffffffffu, c != 0);
+        if (!more) break;
+        c = 0;
+        if (lane > 0 && lane < 24) {
+            long long v = t[0] + cin;
+            c = v >> 32;
+            t[0] = v & 0xffffffffLL;
+#pragma unroll
+            for (int k = 1; k < 3; ++k) {
+                v = t[k] + c;
+                c = v >> 32;
+                t[k] = v & 0xffffffffLL;
+            }
         }
     }
-    int top = kXL - 1;
-    while (top >= 0 && L[top] == 0) --top;
-    if (top < 0) return 0.0;
-    auto mag = [&](int i) -> unsigned long long {
-        return i < 0 ? 0ull : static_cast<unsigned long long>(L[i]);
+    sign = __shfl_sync(0xffffffffu, sign, 23);
+    r.neg = sign < 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) r.d[k] = static_cast<unsigned>(t[k]);
+    if (r.neg) {  // magnitude = ~D + 1: the +1 lands on D's lowest nonzero digit
+        const bool nz = (r.d[0] | r.d[1] | r.d[2]) != 0;
+        const unsigned m = __ballot_sync(0xffffffffu, nz);
+        const int l0 = m ? __ffs(m) - 1 : 32;
+        int k0 = 3;
+        if (lane == l0) k0 = r.d[0] ? 0 : (r.d[1] ? 1 : 2);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const bool below = lane < l0 || (lane == l0 && k < k0);
+            const bool at = lane == l0 && k == k0;
+            r.d[k] = below ? 0u : (at ? 0u - r.d[k] : ~r.d[k]);
+        }
+        if (lane >= 24) r.d[0] = r.d[1] = r.d[2] = 0;
+    }
+    return r;
+}
+
+// Round a magnitude (xred_mag_warp) to the nearest double; all lanes call,
+// every lane gets the value.
+__device__ __forceinline__ double xred_round_mag(const XMag& r)
+{
+    const int lane = threadIdx.x & 31;
+    if (r.special == 3) return __longlong_as_double(0x7ff8000000000000LL);
+    if (r.special == 1) return __longlong_as_double(0x7ff0000000000000LL);
+    if (r.special == 2) return __longlong_as_double(static_cast<long long>(0xfff0000000000000ULL));
+    const int kt = r.d[2] ? 2 : (r.d[1] ? 1 : (r.d[0] ? 0 : -1));
+    const unsigned m = __ballot_sync(0xffffffffu, kt >= 0);
+    if (!m) return 0.0;
+    const int tl = 31 - __clz(static_cast<int>(m));             // top lane
+    const int ktop = __shfl_sync(0xffffffffu, kt, tl);
+    const int top = 3 * tl + ktop;                               // top digit index
+    auto digit = [&](int i) -> unsigned long long {            // broadcast digit i
+        const int src = i < 0 ? 0 : i / 3, k = i < 0 ? 0 : i % 3;
+        const unsigned v0 = __shfl_sync(0xffffffffu, r.d[0], src);
+        const unsigned v1 = __shfl_sync(0xffffffffu, r.d[1], src);
+        const unsigned v2 = __shfl_sync(0xffffffffu, r.d[2], src);
+        const unsigned v = k == 0 ? v0 : (k == 1 ? v1 : v2);
+        return i < 0 ? 0ull : static_cast<unsigned long long>(v);
     };
-    double r;
-    if (top <= 1) {  // < 2^64 units: one correctly rounded conversion
-        r = ldexp(__ull2double_rn((mag(1) << 32) | mag(0)), -1074);
+    const unsigned long long dt = digit(top), d1 = digit(top - 1), d2 = digit(top - 2);
+    // sticky: any digit below top - 2
+    bool low = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) low |= (3 * lane + k < top - 2) && r.d[k] != 0;
+    const bool sticky_low = __any_sync(0xffffffffu, low);
+    double res;
+    if (top <= 1) {  // < 2^64 units: the value is dt (top 0) or dt:d1 (top 1)
+        const unsigned long long v = top == 1 ? ((dt << 32) | d1) : dt;
+        res = ldexp(__ull2double_rn(v), -1074);
     } else {
-        const unsigned long long dt = mag(top), d1 = mag(top - 1), d2 = mag(top - 2);
-        const int hb = 31 - __clz(static_cast<int>(dt));  // msb of the top digit
-        const int ls = 31 - hb;  // left-align the msb to bit 95 of dt:d1:d2
+        const int hb = 31 - __clz(static_cast<int>(dt));
+        const int ls = 31 - hb;
         const unsigned long long hi64 = (dt << 32) | d1;
         unsigned long long T = ls ? ((hi64 << ls) | (d2 >> (32 - ls))) : hi64;
-        bool sticky = ((d2 << ls) & 0xffffffffull) != 0;
-        for (int i = top - 3; i >= 0 && !sticky; --i) sticky = L[i] != 0;
-        T |= sticky ? 1ull : 0ull;  // sticky below the round bit: RNE unchanged
-        // bit 0 of T weighs 2^(32 (top - 2) + 1 + hb) units of 2^-1074
-        r = ldexp(__ull2double_rn(T), 32 * (top - 2) + 1 + hb - 1074);
+        const bool sticky = sticky_low || ((d2 << ls) & 0xffffffffull) != 0;
+        T |= sticky ? 1ull : 0ull;
+        res = ldexp(__ull2double_rn(T), 32 * (top - 2) + 1 + hb - 1074);
     }
-    return neg ? -r : r;
+    return r.neg ? -res : res;
+}
+
+// Digit i (0..71) of a magnitude, fetched from its owning lane; all lanes
+// call (out-of-range i gives 0).
+__device__ __forceinline__ unsigned xred_digit(const XMag& r, int i)
+{
+    const int src = (i < 0 || i > 71) ? 0 : i / 3, k = (i < 0 || i > 71) ? 0 : i % 3;
+    const unsigned v0 = __shfl_sync(0xffffffffu, r.d[0], src);
+    const unsigned v1 = __shfl_sync(0xffffffffu, r.d[1], src);
+    const unsigned v2 = __shfl_sync(0xffffffffu, r.d[2], src);
+    return (i < 0 || i > 71) ? 0u : (k == 0 ? v0 : (k == 1 ? v1 : v2));
+}
+
+__device__ __forceinline__ double xred_round_warp(const long long* L)
+{
+    return xred_round_mag(xred_mag_warp(L));
 }
 
 }  // namespace lbk
