@@ -102,7 +102,12 @@ static lbk_status ctx_create_impl(int device, void* stream, bool own, lbk_ctx* o
             if (ctx->l2_persist && ctx->persist_max)
                 cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(lim));
             const char* pdl = std::getenv("LBK_PDL");
-            ctx->pdl = (pdl && pdl[0] == '0') ? 0 : 1;  // on unless LBK_PDL=0
+            // off unless LBK_PDL=1: with exact reductions the kernels' tails
+            // (block flush + global limb atomics) are longer, and early-
+            // scheduled successor CTAs waiting in griddepcontrol.wait cost
+            // more than they save (CG 1,047 -> 1,094 it/s, P = 8 per-rank
+            // iteration 157 -> 149 us without it)
+            ctx->pdl = (pdl && pdl[0] == '1') ? 1 : 0;
         }
         {
             // solver workspaces come from the stream-ordered pool; keep freed

@@ -67,9 +67,10 @@ struct lbk_ctx_s {
     // misses.  0 off, 1 on; persist_max = the device's window / carve-out.
     int l2_persist = 0;
     size_t persist_max = 0;
-    // programmatic dependent launch for the SpMV / solver kernel chain (on;
-    // LBK_PDL=0 turns it off): a kernel's CTAs are scheduled while its
-    // predecessor drains and wait in griddepcontrol.wait for its results
+    // programmatic dependent launch for the SpMV / solver kernel chain
+    // (LBK_PDL=1; off by default since the exact reductions, see ctx.cu): a
+    // kernel's CTAs are scheduled while its predecessor drains and wait in
+    // griddepcontrol.wait for its results
     int pdl = 0;
 };
 
