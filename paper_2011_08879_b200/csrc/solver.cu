@@ -1188,12 +1188,13 @@ struct LocalEnv {
     long long n_global() const { return n; }
     long long nnz_global() const { return nnz; }
     bool ext_x() const { return false; }
-    // single GPU: 3-5 long kernels per iteration, launch gaps are noise;
-    // LBK_SOLVER_GRAPH=1 turns capture on (tests the path)
+    // chunks after the first replay as a captured CUDA graph (round 2: on by
+    // default -- with PDL off the launch gaps show, CG +0.6%, the
+    // recurrence stop +1.2%); LBK_SOLVER_GRAPH=0 launches eagerly
     bool graph_ok() const
     {
         const char* e = std::getenv("LBK_SOLVER_GRAPH");
-        return e && e[0] == '1';
+        return !(e && e[0] == '0');
     }
     template <class Epi>
     void apply(const double* x, const Epi& e) { op.apply(ctx, x, e, ws); }
