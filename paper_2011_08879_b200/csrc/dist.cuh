@@ -104,6 +104,7 @@ struct SubCsr {
 template <class Epi>
 struct MappedEpi {
     static constexpr int NV = Epi::NV;
+    static constexpr unsigned kSq = SqMask<Epi>::value;
     Epi e;
     const int* __restrict__ map;
     struct Pre {
@@ -127,6 +128,7 @@ struct MappedEpi {
 template <class Epi>
 struct OffsetEpiBase {
     static constexpr int NV = Epi::NV;
+    static constexpr unsigned kSq = SqMask<Epi>::value;
     Epi e;
     int off;
     __device__ bool skip() const { return e.skip(); }

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 
 #include "lbk.h"
@@ -258,12 +259,30 @@ __device__ __forceinline__ void terms_zero(Terms<NV>& t)
 #pragma unroll
     for (int k = 0; k < (NV > 0 ? NV : 1); ++k) t.v[k] = 0.0;
 }
-template <int NV>
+// SQ: bit k set when value k is a sum of squares (epilogue / op `kSq`)
+template <unsigned SQ = 0, int NV>
 __device__ __forceinline__ void terms_flush(RAcc* acc, const Terms<NV>& t)
 {
 #pragma unroll
-    for (int k = 0; k < NV; ++k) racc_add(acc, k, t.v[k]);
+    for (int k = 0; k < NV; ++k) {
+        if constexpr (kExactRed) {
+            if ((SQ >> k) & 1u) xl_add<true>(acc[k], t.v[k], xwarp_limbs() + k * kXV);
+            else xl_add<false>(acc[k], t.v[k], xwarp_limbs() + k * kXV);
+        } else {
+            racc_add(acc, k, t.v[k]);
+        }
+    }
 }
+// Epilogues / vector ops whose reduced values are sums of squares declare
+// `static constexpr unsigned kSq` (bit k for value k); default none.
+template <class E, class = void>
+struct SqMask {
+    static constexpr unsigned value = 0;
+};
+template <class E>
+struct SqMask<E, std::void_t<decltype(E::kSq)>> {
+    static constexpr unsigned value = E::kSq;
+};
 
 // Kernel prologue of every reducing kernel (all threads, after any
 // block-uniform early exit): zeroes the block accumulator.

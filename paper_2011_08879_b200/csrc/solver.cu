@@ -110,6 +110,7 @@ __device__ void raise_breakdown(SolverState* st, int what, int iter)
 // axpy(1,b) == b - Ax exactly), copies to p (and rt), <r,r>.
 struct EpiInit {
     static constexpr int NV = 1;
+    static constexpr unsigned kSq = 1;  // <r,r>
     const double* __restrict__ b;
     double* __restrict__ r;
     double* __restrict__ p;
@@ -198,6 +199,7 @@ struct EpiCgK1 {
 // CG K3: true residual (+ fused p = beta p + r for the next iteration).
 struct EpiCgK3 {
     static constexpr int NV = 1;
+    static constexpr unsigned kSq = 1;  // ||t||^2
     const double* __restrict__ b;
     double* __restrict__ p;
     const double* __restrict__ r;
@@ -260,6 +262,7 @@ __device__ void EpiCgK3::finish(const double* tot) const
 // residual_mode 1: stand-alone true residual check (no p update).
 struct EpiTrueRes {
     static constexpr int NV = 1;
+    static constexpr unsigned kSq = 1;
     const double* __restrict__ b;
     SolverState* st;
     struct Pre {
@@ -340,6 +343,7 @@ struct EpiBiB2 {
 // BiCGSTAB B4: t = A s, <t,t>, <t,s>
 struct EpiBiB4 {
     static constexpr int NV = 2;
+    static constexpr unsigned kSq = 1;  // <t,t> (value 0); <t,s> signed
     double* __restrict__ t;
     const double* __restrict__ s;
     SolverState* st;
@@ -379,6 +383,7 @@ struct EpiBiB4 {
 // BiCGSTAB B6: true residual + fused p = (p - w v) beta + r for iter+1.
 struct EpiBiB6 {
     static constexpr int NV = 1;
+    static constexpr unsigned kSq = 1;
     const double* __restrict__ b;
     double* __restrict__ p;
     const double* __restrict__ v;
@@ -519,6 +524,7 @@ struct EpiCgsT {
 
 struct EpiCgsRes {
     static constexpr int NV = 1;
+    static constexpr unsigned kSq = 1;
     const double* __restrict__ b;
     SolverState* st;
     struct Pre {
@@ -586,6 +592,7 @@ __device__ bool gm_step_skip(const SolverState* st, int jj)
 // bits), whose flops are counted when that cycle starts.
 struct EpiGmRes {
     static constexpr int NV = 1;
+    static constexpr unsigned kSq = 1;
     const double* __restrict__ b;
     double* __restrict__ v0;
     SolverState* st;
@@ -740,7 +747,7 @@ __global__ void __launch_bounds__(256, 4) vec_kernel(long long n, Op op, RedWs w
         if constexpr (!NoFinish<Op>::value) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                terms_flush(acc, pend[u]);
+                terms_flush<SqMask<Op>::value>(acc, pend[u]);
                 pend[u] = t[u];
             }
         }
@@ -750,12 +757,12 @@ __global__ void __launch_bounds__(256, 4) vec_kernel(long long n, Op op, RedWs w
         Terms<NV> t;
         terms_zero(t);
         op.elem(i0, in, &t);
-        if constexpr (!NoFinish<Op>::value) terms_flush(acc, t);
+        if constexpr (!NoFinish<Op>::value) terms_flush<SqMask<Op>::value>(acc, t);
     }
     if constexpr (!NoFinish<Op>::value) {
 #pragma unroll 1
         for (int u = 0; u < U; ++u) {
-            terms_flush(acc, pend[0]);
+            terms_flush<SqMask<Op>::value>(acc, pend[0]);
 #pragma unroll
             for (int k = 0; k + 1 < U; ++k) pend[k] = pend[k + 1];
         }
@@ -769,6 +776,7 @@ __global__ void __launch_bounds__(256, 4) vec_kernel(long long n, Op op, RedWs w
 // CG K2: x += alpha p; r -= alpha q; <r,r>; beta = <r,r>/rho (for K3).
 struct OpCgK2 {
     static constexpr int NV = 1;
+    static constexpr unsigned kSq = 1;  // <r,r>
     double* __restrict__ x;
     double* __restrict__ r;
     const double* __restrict__ p;
@@ -840,6 +848,7 @@ struct OpCgP {
 // BiCGSTAB B3: s = r - alpha v; <s,s>
 struct OpBiB3 {
     static constexpr int NV = 1;
+    static constexpr unsigned kSq = 1;  // <s,s>
     double* __restrict__ s;
     const double* __restrict__ r;
     const double* __restrict__ v;
@@ -1426,6 +1435,7 @@ __global__ void peer_xflush_cg_kernel(E3 e3, long long* s3, PeerDev pd)
 // ||b|| of the distributed right-hand side (exact mode)
 struct OpSelfDot {
     static constexpr int NV = 1;
+    static constexpr unsigned kSq = 1;
     const double* __restrict__ b;
     __device__ bool skip() const { return false; }
     __device__ void prologue() {}

@@ -371,7 +371,7 @@ __device__ __forceinline__ void staged_rows(int rb, int re, T* sv, const int* sc
 #pragma unroll
             for (int q = 0; q < G; ++q) {
                 if constexpr (kPipe) {  // the previous pass's terms, under the gathers
-                    terms_flush(acc, pend[q]);
+                    terms_flush<SqMask<Epi>::value>(acc, pend[q]);
                     terms_zero(pend[q]);
                 }
             }
@@ -392,7 +392,7 @@ __device__ __forceinline__ void staged_rows(int rb, int re, T* sv, const int* sc
         if constexpr (kPipe) {
 #pragma unroll
             for (int q = 0; q < G; ++q) {
-                terms_flush(acc, pend[q]);
+                terms_flush<SqMask<Epi>::value>(acc, pend[q]);
                 terms_zero(pend[q]);
             }
         }
@@ -667,7 +667,7 @@ __global__ void __launch_bounds__((StreamCfg<T, 1>::kThreads), LBK_CSR_MINB)
 
     if constexpr (kExactRed && Epi::NV == 1) {
 #pragma unroll
-        for (int q = 0; q < G; ++q) terms_flush(acc, pend[q]);
+        for (int q = 0; q < G; ++q) terms_flush<SqMask<Epi>::value>(acc, pend[q]);
     }
     if constexpr (Epi::NV > 0) {
         __syncthreads();
@@ -865,7 +865,7 @@ __global__ void __launch_bounds__((StreamCfg<T, 2>::kThreads), 2)
 
     if constexpr (kExactRed && Epi::NV == 1) {
 #pragma unroll
-        for (int q = 0; q < G; ++q) terms_flush(acc, pend[q]);
+        for (int q = 0; q < G; ++q) terms_flush<SqMask<Epi>::value>(acc, pend[q]);
     }
     if constexpr (Epi::NV > 0) {
         __syncthreads();

@@ -201,6 +201,8 @@ __device__ __forceinline__ void xl_direct(unsigned long long m, int pos, bool ne
 }
 
 // Add one term.  `limbs` = this value's flush target (the warp's limbs).
+// NN: the caller guarantees v >= 0 (a square): no two's-complement path.
+template <bool NN = false>
 __device__ __forceinline__ void xl_add(XLane& a, double v, long long* limbs)
 {
     const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
@@ -236,14 +238,19 @@ __device__ __forceinline__ void xl_add(XLane& a, double v, long long* limbs)
     const int u = hi ? s - 64 : s;
     const unsigned long long lo_w = m << u;
     const unsigned long long hi_w = u ? (m >> (64 - u)) : 0ull;
-    const unsigned long long sg = static_cast<unsigned long long>(static_cast<long long>(bits) >> 63);
-    const unsigned long long t0 = (hi ? 0ull : lo_w) ^ sg;
-    const unsigned long long t1 = (hi ? lo_w : hi_w) ^ sg;
-    const unsigned long long t2 = (hi ? hi_w : 0ull) ^ sg;
-    asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u64 %2, %2, %5;\n\t"
-        "add.cc.u64 %0, %0, %6;\n\taddc.cc.u64 %1, %1, 0;\n\taddc.u64 %2, %2, 0;"
-        : "+l"(a.w0), "+l"(a.w1), "+l"(a.w2)
-        : "l"(t0), "l"(t1), "l"(t2), "l"(sg & 1ull));
+    if constexpr (NN) {
+        add192(a, hi ? 0ull : lo_w, hi ? lo_w : hi_w, hi ? hi_w : 0ull);
+    } else {
+        const unsigned long long sg =
+            static_cast<unsigned long long>(static_cast<long long>(bits) >> 63);
+        const unsigned long long t0 = (hi ? 0ull : lo_w) ^ sg;
+        const unsigned long long t1 = (hi ? lo_w : hi_w) ^ sg;
+        const unsigned long long t2 = (hi ? hi_w : 0ull) ^ sg;
+        asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u64 %2, %2, %5;\n\t"
+            "add.cc.u64 %0, %0, %6;\n\taddc.cc.u64 %1, %1, 0;\n\taddc.u64 %2, %2, 0;"
+            : "+l"(a.w0), "+l"(a.w1), "+l"(a.w2)
+            : "l"(t0), "l"(t1), "l"(t2), "l"(sg & 1ull));
+    }
 }
 
 // Zero the block accumulator; every thread of the block must call.
