@@ -374,8 +374,8 @@ lbk_status lbk_comm_init_threads(int32_t nranks, lbk_comm* comms_out /* [nranks]
 /* Peer-memory group (new; csrc/peer.cuh): every rank maps every peer's
  * device window, and the halo exchange and the solver's scalar reductions
  * run as lbk's own kernels storing over NVLink -- no NCCL on the iteration
- * path, CUDA-graph capturable, reductions summed in rank order (same bits
- * on every rank).  halo_cap = the largest per-peer ghost count of any rank
+ * path, CUDA-graph capturable, the solver's reductions exactly rounded
+ * over all ranks (same bits on every rank and at every rank count).  halo_cap = the largest per-peer ghost count of any rank
  * (equal on all ranks).  One process per GPU: init, publish the 64-byte
  * IPC handle over the caller's bootstrap, open all handles (nranks x 64
  * bytes, in rank order).  In-process: lbk_comm_init_peer_group, one
@@ -409,9 +409,11 @@ lbk_status lbk_dist_csr_destroy(lbk_dist_csr D);
  * interior rows -> boundary rows.  Collective: every rank calls it, on the
  * same context stream every time (the peer epochs are per stream order). */
 lbk_status lbk_dist_spmv_f64(lbk_ctx ctx, lbk_dist_csr D, lbk_comm comm, double* x_ext, double* y);
-/* Distributed solve (CG / BiCGSTAB, lbk_solver_cfg as lbk_solve_csr): b, x
- * are the rank's n_local parts; dot products are reduced over ranks, so
- * every rank sees the same iterations, history and result.  Collective. */
+/* Distributed solve (CG / BiCGSTAB / CGS / GMRES, lbk_solver_cfg as
+ * lbk_solve_csr): b, x are the rank's n_local parts.  Dot products are
+ * exactly rounded over all ranks, so every rank sees the same iterations,
+ * history and result -- and they are the single-GPU lbk_solve_csr bits for
+ * any number of ranks and any row partition.  Collective. */
 lbk_status lbk_dist_solve(lbk_ctx ctx, lbk_dist_csr D, lbk_comm comm, const double* b, double* x,
                           const lbk_solver_cfg* cfg, lbk_solve_result* result, double* history,
                           int32_t history_cap);

@@ -150,9 +150,10 @@ struct NcclComm final : Comm {
 // the same or on different devices), meet at host barriers.  Used for
 // P virtual ranks on one GPU (the partition / halo / reduction logic runs
 // exactly as with NCCL) and for single-process multi-GPU runs.  Allreduce
-// sums the per-rank values in rank order on the host, so every rank gets
-// the same bits; exchanges are device-to-device copies from the peers'
-// send buffers.
+// sums the per-rank values on the host (exact int64 limbs for the solver's
+// reductions, allreduce_i64; doubles in rank order for the public
+// allreduce_sum), so every rank gets the same bits; exchanges are
+// device-to-device copies from the peers' send buffers.
 struct ThreadShared {
     int P;
     std::barrier<> bar;

@@ -18,7 +18,9 @@
 //            back (`empty` word in the sender's window).
 //   scalars  the finishing kernel of each fused reduction posts the rank's
 //            totals into every window's mailbox, waits for all P posts and
-//            sums them in rank order -- the same bits on every rank -- then
+//            sums them (exact integer limbs, xred.cuh; the double mailbox is
+//            the -DLBK_RED_TREE build's rank-ordered sum) -- the same bits on
+//            every rank and at every rank count -- then
 //            advances the solver recurrence (combine + allreduce + finish
 //            in one launch).
 //
