@@ -297,6 +297,8 @@ struct PeerComm final : Comm {
         pd.P = P;
         pd.rank = r;
         pd.cap = cap;
+        const char* xd = std::getenv("LBK_XRED_DIGITS");
+        pd.xdigits = (xd && xd[0] == '1') ? 1 : 0;
         pd.win[r] = local;
     }
     // every window must use the same slot capacity (senders index the

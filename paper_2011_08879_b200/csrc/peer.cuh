@@ -68,6 +68,8 @@ struct PeerDev {
     PeerHdr* win[kPeerMax];
     int P = 0, rank = 0;
     long long cap = 0;
+    int xdigits = 0;  // LBK_XRED_DIGITS=1: post normalised digits always (tests
+                      // the wide-range encoding on ordinary data)
     // staging slot (parity par, source src) inside rank q's window
     __device__ unsigned long long* stage(int q, int par, int src) const
     {
@@ -255,7 +257,7 @@ __device__ __forceinline__ void peer_xallreduce_warp(const PeerDev& pd, long lon
         const int cnt = h0 < 0 ? 0 : h0 - l0 + 1;
         const unsigned fl = (X[kXPinf] ? 1u << 17 : 0u) | (X[kXNinf] ? 1u << 18 : 0u) |
                             (X[kXNan] ? 1u << 19 : 0u);
-        if (2 * cnt + 1 <= kXV) {
+        if (2 * cnt + 1 <= kXV && !pd.xdigits) {
             lo_l[v] = h0 < 0 ? 0 : l0;
             hdr[v] = static_cast<unsigned>(lo_l[v]) | (static_cast<unsigned>(cnt) << 8) | fl |
                      (1u << 20);

@@ -113,6 +113,11 @@ def main():
     out["bicgstab_unmerged"] = solve("bicgstab", A, b)
     os.environ.pop("LBK_CG_MERGE")
     out["bicgstab_fixed"] = solve("bicgstab", A, b, fixed=23)
+    # the exact exchange's wide-range encoding (sign-magnitude digits) on
+    # ordinary data: the same bits as the raw-limb posts
+    os.environ["LBK_XRED_DIGITS"] = "1"
+    out["bicgstab_digits"] = solve("bicgstab", A, b)
+    os.environ.pop("LBK_XRED_DIGITS")
     A = O.stencil("7pt", 14, 0.5)
     b = O.spmv_csr(A, O.seeded_values(A.nrows, 11))
     out["cgs"] = solve("cgs", A, b)

@@ -241,6 +241,8 @@ def test_peer_solvers(peer_run, O):
     # captured graph and eager launches give the same bits
     assert out[0]["bicgstab"]["hist"] == out[0]["bicgstab_eager"]["hist"]
     assert out[0]["bicgstab"]["hist"] == out[0]["bicgstab_unmerged"]["hist"]
+    assert out[0]["bicgstab"]["hist"] == out[0]["bicgstab_digits"]["hist"]
+    assert out[0]["bicgstab"]["x"] == out[0]["bicgstab_digits"]["x"]
     assert out[0]["bicgstab"]["x"] == out[0]["bicgstab_unmerged"]["x"]
     assert out[0]["bicgstab_fixed"]["iters"] == 23
     assert len(out[0]["bicgstab_fixed"]["hist"]) == 24
