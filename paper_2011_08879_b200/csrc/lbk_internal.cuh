@@ -195,10 +195,26 @@ __device__ __forceinline__ void l2_prefetch_rows(const double* v, int rb, int re
         asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 
+// Gathers of x.  -DLBK_GATHER_NOALLOC / -DLBK_GATHER_CG select the
+// L1::no_allocate or L2-only (.cg) forms for A/B measurements.
 template <typename T>
 __device__ __forceinline__ T ldg_nc(const T* p)
 {
+#if defined(LBK_GATHER_NOALLOC)
+    if constexpr (sizeof(T) == 8) {
+        double v;
+        asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+        return static_cast<T>(v);
+    } else {
+        float v;
+        asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+        return static_cast<T>(v);
+    }
+#elif defined(LBK_GATHER_CG)
+    return __ldcg(p);
+#else
     return __ldg(p);
+#endif
 }
 
 // Exact-rounding arithmetic helpers: products and sums are rounded
