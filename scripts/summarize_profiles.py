@@ -113,6 +113,44 @@ def cg_full():
     open(os.path.join(P, f"r{rnd}_cg_kernels_ncu.txt"), "w").write("\n".join(lines) + "\n")
 
 
+def cfg3_full():
+    """cfg3 power-law captures (TAG_pl_{csr,coo,f32}.ncu-rep, one launch each,
+    scripts/prof_pl.py) -> rROUND_cfg3_ncu.txt and ncu_summary.json entries."""
+    n, nnz = 1 << 24, 268_195_029
+    alg = {"csr": 12 * nnz + 4 * (n + 1) + 16 * n, "coo": 16 * nnz + 16 * n,
+           "f32": 8 * nnz + 4 * (n + 1) + 8 * n}
+    lines = ["# ncu --set full --clock-control none -k regex:'csr_stream|coo_stream' -c 1 "
+             "python scripts/prof_pl.py {csr|coo|f32}: cfg3 power-law (2^24 rows, 268,195,029 "
+             "nnz, max row 10,000), one launch each"]
+    summ = json.load(open(os.path.join(P, "ncu_summary.json")))
+    found = False
+    for w in ("csr", "coo", "f32"):
+        rep = os.path.join(G, f"{tag}_pl_{w}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        found = True
+        (d, u), = raw(rep)[:1]
+        dram = to_bytes(d, u, "dram__bytes_read.sum") + to_bytes(d, u, "dram__bytes_write.sum")
+        dur = float(d["gpu__time_duration.sum"].replace(",", ""))
+        dur_us = dur / 1e3 if u["gpu__time_duration.sum"] == "nsecond" else dur
+        lines.append(f"\n[cfg3 {w}: {d['Kernel Name'][:120]}]")
+        lines += ["  " + fmt(d, u, m) for m in METRICS]
+        lines.append(f"  dram_bytes_total = {int(dram)} B  (traffic / algorithmic = "
+                     f"{dram / alg[w]:.3f})")
+        summ["kernels"][f"cfg3_{w}"] = {
+            "config": f"cfg3 {w}", "kernel": d["Kernel Name"][:120],
+            "dram_bytes_per_launch": int(dram), "algorithmic_bytes_per_launch": alg[w],
+            "ncu_duration_us": dur_us,
+            "warps_active_pct": float(d["sm__warps_active.avg.pct_of_peak_sustained_active"]),
+            "issue_active_pct": float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"]),
+            "l1_lsu_wavefronts_pct": float(
+                d["l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"]),
+            "source": f"profiles/r{rnd}_cfg3_ncu.txt"}
+    if found:
+        open(os.path.join(P, f"r{rnd}_cfg3_ncu.txt"), "w").write("\n".join(lines) + "\n")
+        json.dump(summ, open(os.path.join(P, "ncu_summary.json"), "w"), indent=1)
+
+
 def bench():
     for src, dst in ((f"{tag}_bench.json", f"r{rnd}_bench_N1.json"),
                      (f"{tag}_bench_ref.json", f"r{rnd}_bench_reference_N1.json")):
@@ -122,6 +160,10 @@ def bench():
             json.dump(json.loads(lines[-1]), open(os.path.join(P, dst), "w"), indent=1)
 
 
+if "--cfg3-only" in sys.argv:
+    cfg3_full()
+    print("ok")
+    sys.exit(0)
 launches()
 if "--launches-only" not in sys.argv:
     csr_full()
