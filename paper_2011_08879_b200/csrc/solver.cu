@@ -21,14 +21,16 @@
 // Per-iteration kernels (reference semantics, residual_mode 0):
 //   CG        K1  q = A p            | <p,q>
 //             K2  x += a p, r -= a q  | <r,r>
-//             K3  t = b - A x         | <t,t>   + fused p = beta p + r
+//             K3  t = b - A x         | <t,t>
+//             P   p = beta p + r      (fused into K3 with -DLBK_FUSED_P)
 //   CGS       S1  u, p updates (vec) S2 v = A p | <rt,v>   S3 q, w (vec)
 //             S4  t = A w + x, r updates | <rt,r>    S5 true residual
 //   BiCGSTAB  B2  v = A p            | <rt,v>
 //             B3  s = r - a v         | <s,s>
 //             B4  t = A s            | <t,t>, <t,s>
 //             B5  x += a p + w s; r = s - w t | <rt,r>
-//             B6  t = b - A x         | <t,t>   + fused next p update
+//             B6  t = b - A x         | <t,t>
+//             P   next p update       (fused into B6 with -DLBK_FUSED_P)
 // residual_mode 1 (CG only) drops K3's SpMV: the stopping test uses the
 // recurrence residual sqrt(<r,r>)/||b||, and a true residual is computed
 // and must pass before convergence is declared.
@@ -259,6 +261,41 @@ __device__ void EpiCgK3::finish(const double* tot) const
     cg_after_residual(st, sqrt(tot[0]) / st->norm_b);
 }
 
+// K3 without the fused p update: the true residual alone, then p = beta p
+// + r as its own vector pass (OpCgP).  The default on the unmerged paths:
+// fusing the p update into the SpMV epilogue (EpiCgK3, -DLBK_FUSED_P) adds
+// three operand streams to a latency-bound sweep; split, CG ran 1,115
+// against 1,106 it/s (scripts/gpu_r2ao.sh, two repeats).
+struct EpiCgK3s {
+    static constexpr int NV = 1;
+    static constexpr unsigned kSq = 1;  // ||t||^2
+    const double* __restrict__ b;
+    SolverState* st;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prefetch(int rb, int re) const { l2_prefetch_rows(b, rb, re); }
+    struct Pre {
+        double b;
+    };
+    __device__ Pre pre(int i) const { return {b[i]}; }
+    __device__ void row(int i, double s, auto* acc) const
+    {
+        const double t = add_rn(b[i], -s);
+        racc_add(acc, 0, mul_rn(t, t));
+    }
+    __device__ void row_pre(int, double s, const Pre& pr, auto* acc) const
+    {
+        const double t = add_rn(pr.b, -s);
+        racc_add(acc, 0, mul_rn(t, t));
+    }
+    __device__ void finish(const double* tot) const;
+};
+
+__device__ void EpiCgK3s::finish(const double* tot) const
+{
+    st->flops += 2 * st->nnz + st->n + 2 * st->n + 2 * st->n;  // true_residual
+    cg_after_residual(st, sqrt(tot[0]) / st->norm_b);
+}
+
 // residual_mode 1: stand-alone true residual check (no p update).
 struct EpiTrueRes {
     static constexpr int NV = 1;
@@ -446,6 +483,53 @@ struct EpiBiB6 {
         st->flops += 2 * n + n + 2 * n;
         st->rho = st->rho_next;
     }
+};
+
+// B6 without the fused p update (the default; see EpiCgK3s): the true
+// residual alone, then OpBiP.
+struct EpiBiB6s {
+    static constexpr int NV = 1;
+    static constexpr unsigned kSq = 1;
+    const double* __restrict__ b;
+    SolverState* st;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prefetch(int rb, int re) const { l2_prefetch_rows(b, rb, re); }
+    __device__ void row(int i, double s, auto* acc) const
+    {
+        const double t = add_rn(b[i], -s);
+        racc_add(acc, 0, mul_rn(t, t));
+    }
+    __device__ void finish(const double* tot) const
+    {
+        EpiBiB6{b, nullptr, nullptr, nullptr, st}.finish(tot);
+    }
+};
+
+// BiCGSTAB p = (p - omega v) beta + r (krylov.cpp:199-201), skipped once the
+// solve is over
+struct OpBiP {
+    static constexpr int NV = 1;
+    double* __restrict__ p;
+    const double* __restrict__ v;
+    const double* __restrict__ r;
+    SolverState* st;
+    double beta, omega;
+    __device__ bool skip() const { return *(volatile int*)&st->done != 0; }
+    __device__ void prologue()
+    {
+        beta = st->beta;
+        omega = st->omega;
+    }
+    struct In {
+        double p, v, r;
+    };
+    __device__ In load(long long i) const { return {p[i], v[i], r[i]}; }
+    __device__ void elem(long long i, const In& in, auto*) const
+    {
+        p[i] = add_rn(mul_rn(add_rn(in.p, mul_rn(-omega, in.v)), beta), in.r);
+    }
+    static constexpr bool kNoFinish = true;
+    __device__ void finish(const double*) const {}
 };
 
 // CGS (krylov.cpp:233-297), reference semantics (true residual each
@@ -1861,7 +1945,12 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
             env.apply(p, EpiCgK1{q, p, st});
             env.vec(OpCgK2{x, r, p, q, st, recurrence ? 1 : 0, 0.0});
             if (!recurrence) {
+#ifdef LBK_FUSED_P
                 env.apply(x, EpiCgK3{b, p, r, st});
+#else
+                env.apply(x, EpiCgK3s{b, st});
+                env.vec(OpCgP{p, r, st, 0.0});
+#endif
             } else {
                 env.apply(x, EpiTrueRes{b, st});
                 env.vec(OpCgP{p, r, st, 0.0});
@@ -1881,7 +1970,12 @@ void solve_impl(lbk_ctx ctx, Env& env, const double* b, double* x_user, const lb
             env.vec(OpBiB3{s, r, q, st, 0.0});
             env.apply(s, EpiBiB4{t, s, st});
             env.vec(OpBiB5{x, r, p, s, t, rt, st, 0.0, 0.0});
+#ifdef LBK_FUSED_P
             env.apply(x, EpiBiB6{b, p, q, r, st});
+#else
+            env.apply(x, EpiBiB6s{b, st});
+            env.vec(OpBiP{p, q, r, st, 0.0, 0.0});
+#endif
         }
     };
     // Chunked launch loop; `done` is polled once per chunk.  Where the
